@@ -1,0 +1,350 @@
+"""Pins of the CPU oracle against things other than itself (all CPU, -m "not gpu").
+
+Each test names what fixes the expected value: a printed worked example
+(tests/golden/spec_examples.json, cited), brute-force enumeration, a closed
+form, an invariant, or an LP solved by a different method.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import lp
+from spfom_inputs import Instance, generate
+from tests.pins import kkt_certificate, project_bruteforce
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def rand_segment(rng, k, mnl=False, scale=1.0):
+    v = rng.uniform(0.1, 1.0, k)
+    w = np.zeros(k) if mnl else v * rng.uniform(0.0, 0.5, k)
+    v0 = rng.uniform(0.5, 2.0)
+    lam = rng.uniform(1.0, 10.0)
+    z0 = rng.normal() * lam * scale
+    z = rng.normal(size=k) * lam * scale * rng.uniform(0.0, 1.0)
+    return z0, z, v, w, v0, lam
+
+
+# ------------------------------------------------------------ projection
+@pytest.mark.parametrize("seed", range(4))
+def test_projection_matches_active_set_enumeration(seed):
+    """Pin (i) of c5: KKT active-set enumeration in the original variables, k <= 6."""
+    rng = np.random.default_rng(100 + seed)
+    worst = 0.0
+    for t in range(150):
+        k = int(rng.integers(1, 7))
+        z0, z, v, w, v0, lam = rand_segment(rng, k, mnl=(t % 4 == 0), scale=[0.1, 1.0, 10.0][t % 3])
+        y0, y, _m, _ = oracle.project(z0, z, v, w, v0, lam)
+        b0, by = project_bruteforce(z0, z, v, w, v0, lam)
+        worst = max(worst, abs(y0 - b0) / lam, np.abs(y - by).max() / lam)
+    assert worst <= 1e-13, worst
+
+
+def test_projection_identity_on_feasible_points():
+    """Pin (ii): z in Y_i => Pi(z) = z (feasible points built as convex
+    combinations of assortment vertices, App. A.1)."""
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        k = int(rng.integers(1, 12))
+        _z0, _z, v, w, v0, lam = rand_segment(rng, k)
+        vt0 = v0 + w.sum()
+        y = np.zeros(k)
+        wts = rng.dirichlet(np.ones(4))
+        for a in wts:
+            S = rng.random(k) < 0.5
+            U = lam / (vt0 + (v - w)[S].sum())
+            y += a * np.where(S, v * U, 0.0)
+        y0 = lam - y.sum()
+        p0, p, _m, _ = oracle.project(y0, y, v, w, v0, lam)
+        assert abs(p0 - y0) <= 1e-13 * lam and np.abs(p - y).max() <= 1e-13 * lam
+
+
+def test_projection_k1_closed_form():
+    """Pin (iv): for k = 1 the GAM polytope is the segment between (lam, 0) and
+    (lam v0/(v0+v), lam v/(v0+v)) (GAM reduces to MNL at k = 1: y/v <= y0/v0),
+    so the projection is the closed-form projection onto that segment."""
+    rng = np.random.default_rng(11)
+    for _ in range(500):
+        z0, z, v, w, v0, lam = rand_segment(rng, 1, scale=3.0)
+        A = np.array([lam, 0.0])
+        Bp = np.array([lam * v0[()] if np.ndim(v0) else lam * v0, lam * v[0]]) / (v0 + v[0])
+        d = Bp - A
+        tt = np.clip(((np.array([z0, z[0]]) - A) @ d) / (d @ d), 0.0, 1.0)
+        ref = A + tt * d
+        y0, y, _m, _ = oracle.project(z0, z, v, w, v0, lam)
+        assert abs(y0 - ref[0]) <= 1e-13 * lam and abs(y[0] - ref[1]) <= 1e-13 * lam
+
+
+def test_projection_scaling_and_nonexpansive():
+    """Pins (v) Pi_{lam Y1}(z) = lam Pi_{Y1}(z/lam) and (vi) ||Pi(z)-Pi(z')|| <= ||z-z'||."""
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        k = int(rng.integers(1, 40))
+        z0, z, v, w, v0, lam = rand_segment(rng, k)
+        y0, y, _m, _ = oracle.project(z0, z, v, w, v0, lam)
+        u0, u, _m, _ = oracle.project(z0 / lam, z / lam, v, w, v0, 1.0)
+        assert abs(y0 - lam * u0) <= 1e-12 * lam and np.abs(y - lam * u).max() <= 1e-12 * lam
+        dz0, dz = rng.normal() * 0.3, rng.normal(size=k) * 0.3
+        q0, q, _m, _ = oracle.project(z0 + dz0, z + dz, v, w, v0, lam)
+        lhs = np.hypot(q0 - y0, np.linalg.norm(q - y))
+        rhs = np.hypot(dz0, np.linalg.norm(dz))
+        assert lhs <= rhs * (1 + 1e-12) + 1e-13
+
+
+@pytest.mark.parametrize("k", [50, 200])
+def test_projection_kkt_certificate_large_k(k):
+    """Pin at any k: NNLS-recovered multipliers prove the oracle's point is the
+    projection (stationarity, feasibility, multiplier signs)."""
+    rng = np.random.default_rng(k)
+    for t in range(20):
+        z0, z, v, w, v0, lam = rand_segment(rng, k, scale=[0.05, 1.0, 20.0][t % 3])
+        y0, y, _m, _ = oracle.project(z0, z, v, w, v0, lam)
+        stat, primal, mmin = kkt_certificate(z0, z, v, w, v0, lam, y0, y)
+        assert stat <= 1e-11 and primal <= 1e-12 and mmin >= -1e-12, (stat, primal, mmin)
+
+
+def test_projection_theta_limit_is_argmax():
+    """Pin (iii): Pi(y + theta g) -> argmax_{Y} g^T y as theta -> inf (unique argmax)."""
+    rng = np.random.default_rng(5)
+    for _ in range(100):
+        k = int(rng.integers(1, 30))
+        _z0, _z, v, w, v0, lam = rand_segment(rng, k)
+        g = rng.lognormal(3.0, 0.5, k) - rng.uniform(0, 30, k)
+        val, a0, ay, margin = oracle.argmax(g, v, w, v0, lam)
+        if margin < 1e-3:
+            continue
+        # beyond a finite theta the projection lands exactly on the argmax vertex
+        # (g lies inside that vertex's normal cone); 1e6 * |g| keeps rounding at ~1e-9
+        y0, y, _m, _ = oracle.project(lam, 1e6 * g, v, w, v0, lam)
+        assert np.abs(y - ay).max() <= 1e-8 * lam and abs(y0 - a0) <= 1e-8 * lam
+
+
+# ------------------------------------------------------------ argmax
+def test_argmax_matches_assortment_enumeration():
+    """Pin of c6: max over all 2^k assortments of lam sum_j g_j pi_j(S) (CBLP
+    single segment, P:L211-219 with GAM pi), k <= 10."""
+    rng = np.random.default_rng(21)
+    for t in range(300):
+        k = int(rng.integers(1, 11))
+        _z0, _z, v, w, v0, lam = rand_segment(rng, k, mnl=(t % 3 == 0))
+        g = rng.normal(size=k) * 10
+        val, y0, y, _mg = oracle.argmax(g, v, w, v0, lam)
+        ref = lp.best_assortment_value(g, v, w, v0, lam)
+        assert abs(val - ref) <= 1e-13 * max(1.0, abs(ref))
+        # the returned point is feasible and attains the value
+        assert abs(y0 + y.sum() - lam) <= 1e-13 * lam
+        assert abs(float(g @ y) - val) <= 1e-12 * max(1.0, abs(val))
+
+
+def test_argmax_tie_example():
+    for ex in GOLD["argmax_tie"]:
+        val, y0, y, margin = oracle.argmax(ex["g"], ex["v"], ex["w"], ex["v0"], ex["lam"])
+        assert val == pytest.approx(ex["value"], abs=1e-15)
+        assert np.allclose(y, ex["y"], atol=1e-15) and y0 == pytest.approx(ex["y0"], abs=1e-15)
+        assert margin == 0.0
+
+
+def test_argmax_agrees_with_paper_algorithm_1_golden_section():
+    """MNL: the paper's own inner solver (FAST-INNER + golden section)
+    converges to the exact argmax value as its tolerance shrinks."""
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        k = int(rng.integers(1, 20))
+        _z0, _z, v, _w, v0, lam = rand_segment(rng, k, mnl=True)
+        g = rng.normal(size=k) * 5
+        val, *_ = oracle.argmax(g, v, np.zeros(k), v0, lam)
+        gv, gy0, gy = oracle.golden(g, v, v0, lam, tol=1e-12)
+        assert abs(gv - val) <= 1e-8 * max(1.0, abs(val))
+        assert gv <= val + 1e-12 * max(1.0, abs(val))        # golden is a feasible point
+
+
+# ------------------------------------------------------------ SPEC worked examples
+def test_spec_fast_inner_examples():
+    for ex in GOLD["fast_inner"]:
+        z, y = oracle.fast_inner(ex["g"], ex["v"], ex["v0"], ex["lam"], ex["y0"])
+        assert z == pytest.approx(ex["z"], abs=1e-14), ex["cite"]
+        assert np.allclose(y, ex["y"], atol=1e-14), ex["cite"]
+
+
+def test_spec_feasible_bound_examples():
+    for ex in GOLD["feasible_bound"]:
+        g = np.ones(len(ex["v"]))
+        z, _ = oracle.fast_inner(g, ex["v"], ex["v0"], ex["lam"], ex["bound"] * (1 + 1e-12))
+        assert np.isfinite(z), ex["cite"]
+        z, _ = oracle.fast_inner(g, ex["v"], ex["v0"], ex["lam"], ex["bound"] * (1 - 1e-6))
+        assert np.isnan(z), ex["cite"]
+
+
+def test_spec_golden_examples():
+    for ex in GOLD["golden"]:
+        # value at a kink converges linearly in the bracket width
+        val, y0, _y = oracle.golden(ex["g"], ex["v"], ex["v0"], ex["lam"], tol=1e-9)
+        assert val == pytest.approx(ex["value"], abs=1e-6), ex["cite"]
+
+
+def test_spec_dual_step_examples():
+    for ex in GOLD["dual_step"]:
+        out = oracle.dual_step([ex["eta"]], [ex["s"]], [ex["s"]], [ex["c"]], [ex["tau"]], ex["mu"], 0.0)
+        assert out[0] == pytest.approx(ex["out"], abs=1e-15), ex["cite"]
+
+
+def test_dual_step_extrapolation_hand_example():
+    """st = s + omega (s - s_prev) = 2 + 1*(2 - 1.5) = 2.5 -> 0.2 - 0.1 (1 - 2.5) = 0.35."""
+    out = oracle.dual_step([0.2], [2.0], [1.5], [1.0], [0.1], 0.0, 1.0)
+    assert out[0] == pytest.approx(0.35, abs=1e-15)
+
+
+def _inst(seg_ptr, prod, v, w, v0, lam, r, c):
+    N = len(r)
+    prod = np.asarray(prod, dtype=np.int32)
+    return Instance("hand", np.asarray(seg_ptr, dtype=np.int64), prod, np.asarray(v, float),
+                    np.asarray(w, float), np.asarray(v0, float), np.asarray(lam, float),
+                    np.asarray(r, float), np.asarray(c, float),
+                    np.bincount(prod, minlength=N) > 0, {})
+
+
+def test_spec_compute_R():
+    ex = GOLD["compute_R"][0]
+    inst = _inst([0, 2, 4], [0, 1, 0, 1], ex["v_rows"][0] + ex["v_rows"][1], [0] * 4, [1, 1], [1, 1],
+                 ex["r"], [1, 1])
+    R = oracle.compute_R(inst)
+    assert R == pytest.approx(ex["R"], abs=1e-15) and 1 / (2 * R) == pytest.approx(ex["mu"])
+
+
+@pytest.mark.parametrize("ex", GOLD["sblp_1x1"], ids=lambda e: e["cite"])
+def test_spec_sblp_1x1(ex):
+    """n = m = 1 SBLP optimum: dense simplex, HiGHS and SPFOM (converge preset) agree with S:L458-460."""
+    inst = _inst([0, 1], [0], [ex["v"]], [0.0], [ex["v0"]], [ex["lam"]], [ex["r"]], [ex["c"]])
+    assert lp.sblp_dense(inst)[0] == pytest.approx(ex["obj"], abs=1e-12)
+    assert lp.sblp_highs(inst)[0] == pytest.approx(ex["obj"], abs=1e-9)
+    S = oracle.OracleSolver(inst, theta=1.0, tau=0.9, tau_mode=1, mu=0.0, extrapolation=1.0)
+    S.run(3000)
+    assert S.residuals()["primal_obj"] == pytest.approx(ex["obj"], abs=1e-9)
+    assert S.y[0] == pytest.approx(ex["y"], abs=1e-9)
+
+
+def test_spec_choice_probabilities():
+    for ex in GOLD["choice_prob"]:
+        pi = lp.gam_choice_prob(np.array(ex["v"]), np.array(ex["w"]), ex["v0"], ex["S"])
+        assert np.allclose(pi, ex["pi"], atol=1e-15), ex["cite"]
+
+
+# ------------------------------------------------------------ LP references
+def test_tiny_sblp_equals_cblp_enumeration():
+    """c3/c12: dense simplex SBLP = HiGHS SBLP = CBLP enumeration LP (dense and
+    HiGHS), capacitated and uncapacitated; uncapacitated also = sum of per-segment
+    best assortments."""
+    for seed in (1, 11, 12):
+        inst = generate("tiny", seed=seed)
+        for unc in (False, True):
+            a = lp.sblp_dense(inst, uncapacitated=unc)[0]
+            b = lp.sblp_highs(inst, uncapacitated=unc)[0]
+            c = lp.cblp_lp(inst, uncapacitated=unc)
+            d = lp.cblp_lp(inst, uncapacitated=unc, solver="highs")
+            assert max(abs(a - b), abs(a - c), abs(a - d)) <= 1e-9 * abs(a)
+            if unc:
+                e = sum(lp.best_assortment_value(inst.price[inst.prod_idx[inst.row(i)]],
+                                                 inst.attract[inst.row(i)], inst.shadow[inst.row(i)],
+                                                 inst.no_purchase[i], inst.arrival[i])
+                        for i in range(inst.m))
+                assert abs(a - e) <= 1e-9 * abs(a)
+
+
+# ------------------------------------------------------------ the iteration
+def _check_state_invariants(S, inst):
+    res = S.residuals()
+    assert res["balance_rel_max"] <= 1e-13 and res["scale_rel_max"] <= 1e-13 and res["neg_max"] == 0.0
+    assert (S.eta >= 0).all()
+    fresh = np.bincount(inst.prod_idx, weights=S.y, minlength=inst.N)
+    assert np.abs(fresh - S.s).max() <= 1e-12 * max(1.0, np.abs(fresh).max())
+
+
+def test_oracle_iterates_stay_feasible_and_usage_consistent():
+    inst = generate("small", m=300, N=200, k=30)
+    S = oracle.OracleSolver(inst)
+    for _ in range(30):
+        S.step()
+        _check_state_invariants(S, inst)
+
+
+@pytest.mark.parametrize("seed", [1, 11, 12, 13, 14])
+def test_converge_preset_reaches_tiny_lp_optimum(seed):
+    """c8/c11: converge preset (theta=1, tau_j = 0.9/n_j, omega_x = 1, mu = 0, full
+    sweep), 2000 iterations, vs the dense-simplex P*: <= 1e-9 relative, infeasible <= 1e-9."""
+    inst = generate("tiny", seed=seed)
+    Pstar = lp.sblp_dense(inst)[0]
+    S = oracle.OracleSolver(inst)
+    S.run(2000)
+    res = S.residuals()
+    assert abs(res["primal_obj"] - Pstar) <= 1e-9 * Pstar
+    assert res["infeas_rel"] <= 1e-9
+    assert res["cert_lower"] <= Pstar * (1 + 1e-12) and Pstar <= res["cert_upper"] * (1 + 1e-12)
+
+
+def test_dual_bound_is_weak_duality_upper_bound():
+    """D(eta) >= P* for any eta >= 0 (A.3), here random eta on tiny."""
+    inst = generate("tiny")
+    Pstar = lp.sblp_dense(inst)[0]
+    S = oracle.OracleSolver(inst)
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        eta = rng.uniform(0, 10, inst.N) * (rng.random(inst.N) < 0.7)
+        assert S.residuals(eta=eta)["dual_obj"] >= Pstar - 1e-12 * Pstar
+
+
+def test_sampled_mode_touches_only_block_rows_and_tracks_usage():
+    """c2/c7: with a sampled block only the block's rows change, s is the
+    incremental stale-inclusive sum and equals a fresh recompute."""
+    from spfom_inputs import block_sequence
+    inst = generate("small", m=400, N=150, k=20)
+    blocks = block_sequence(inst.m, 37, 40, seed=5)
+    S = oracle.OracleSolver(inst, theta=np.inf, tau=0.1, tau_mode=0, mu=0.5, extrapolation=0.0)
+    for t in range(40):
+        y_before = S.y.copy()
+        S.step(blocks[t])
+        changed_rows = set(np.searchsorted(inst.seg_ptr, np.flatnonzero(S.y != y_before), side="right") - 1)
+        assert changed_rows <= set(blocks[t].tolist())
+        _check_state_invariants(S, inst)
+
+
+def test_paper_preset_first_iteration_closed_form():
+    """theta = inf from eta = 0: every row is its unconstrained best assortment
+    (enumeration), then eta = max(0, -tau (c - s)) (Alg. 2)."""
+    inst = generate("tiny")
+    S = oracle.OracleSolver(inst, theta=np.inf, tau=0.1, tau_mode=0, mu=0.0, extrapolation=0.0)
+    S.step()
+    for i in range(inst.m):
+        sl = inst.row(i)
+        ref = lp.best_assortment_value(inst.price[inst.prod_idx[sl]], inst.attract[sl], inst.shadow[sl],
+                                       inst.no_purchase[i], inst.arrival[i])
+        assert float(inst.price[inst.prod_idx[sl]] @ S.y[sl]) == pytest.approx(ref, rel=1e-13)
+    s = np.bincount(inst.prod_idx, weights=S.y, minlength=inst.N)
+    assert np.allclose(S.eta, np.maximum(0.0, -0.1 * (inst.capacity - s)), rtol=0, atol=1e-14)
+
+
+def test_averaging_is_uniform_mean_of_iterates():
+    """a8 (reading c9): the running average equals the mean of the stored iterates."""
+    inst = generate("small", m=100, N=60, k=10)
+    A = oracle.OracleSolver(inst, averaging=True)
+    B = oracle.OracleSolver(inst)
+    ys, etas = [], []
+    for _ in range(25):
+        A.step()
+        B.step()
+        ys.append(B.y.copy())
+        etas.append(B.eta.copy())
+    assert np.abs(A.ybar - np.mean(ys, axis=0)).max() <= 1e-13 * max(1, np.abs(A.ybar).max())
+    assert np.abs(A.etabar - np.mean(etas, axis=0)).max() <= 1e-13 * max(1, np.abs(A.etabar).max())
+
+
+def test_multi_period_T1_and_stacking():
+    """c15: T = 1 multi-period == single period; stacked P* == sum over the
+    period LP with shared capacities solved directly (dense simplex on the
+    stacked rows == HiGHS on the same)."""
+    a = generate("multi", m=3, N=5, k=3, T=1)
+    b = generate("multi", m=3, N=5, k=3, T=2)
+    assert b.m == 2 * a.m and np.array_equal(b.prod_idx[: a.nnz], a.prod_idx)
+    assert lp.sblp_dense(b)[0] == pytest.approx(lp.sblp_highs(b)[0], rel=1e-9)
