@@ -1,0 +1,848 @@
+// spfom.cu -- host side of the C ABI declared in include/spfom.h.
+//
+// create: validate (S:L34-36 + GAM rules) -> global column counts n_j (NCCL
+// allreduce when world > 1) -> popularity relabelling of products (descending
+// n_j) -> padded quad CSR (rows sorted by new id, padded to 4 entries with
+// inert pads: v = omega = y = 0, id = N) -> length bins -> copy into the
+// caller's workspace -> initial state (reading c10).
+// step: CUDA-graph replay of one iteration (K1 per bin -> NCCL allreduce of
+// the usage accumulator -> K3 [-> averaging] -> tick).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "spfom.h"
+#include "spfom_kernels.cuh"
+
+using namespace spfom;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+typedef int nccl_res;                       // ncclResult_t
+typedef struct { char internal[128]; } nccl_uid;
+typedef void *nccl_comm;
+enum { kNcclInt64 = 4, kNcclFloat64 = 8 };  // ncclDataType_t
+enum { kNcclSum = 0, kNcclMax = 2 };        // ncclRedOp_t
+
+struct NcclApi {
+    bool ok = false;
+    nccl_res (*GetUniqueId)(nccl_uid *) = nullptr;
+    nccl_res (*CommInitRank)(nccl_comm *, int, nccl_uid, int) = nullptr;
+    nccl_res (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    nccl_res (*CommDestroy)(nccl_comm) = nullptr;
+    const char *(*GetErrorString)(nccl_res) = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.GetUniqueId = (nccl_res(*)(nccl_uid *))dlsym(h, "ncclGetUniqueId");
+        api.CommInitRank = (nccl_res(*)(nccl_comm *, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+        api.AllReduce = (nccl_res(*)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+        api.CommDestroy = (nccl_res(*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+        api.GetErrorString = (const char *(*)(nccl_res))dlsym(h, "ncclGetErrorString");
+        api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    });
+    return api;
+}
+
+thread_local std::string g_create_error;
+
+// Bin = (G lanes per segment, Q quads per lane) -> capacity 4 G Q entries.
+struct BinCfg { int G, Q; };
+constexpr BinCfg kBins[] = {{4, 1}, {4, 2}, {8, 2}, {16, 2}, {32, 2}, {32, 4}, {32, 8}};
+constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
+constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
+
+int bin_of(int64_t nq) {
+    for (int b = 0; b < kNumBins; ++b)
+        if (nq <= (int64_t)kBins[b].G * kBins[b].Q) return b;
+    return -1;
+}
+
+constexpr int kResidBlocks = 592;   // 4 x 148 SMs
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Plan {
+    int64_t m = 0, N = 0, nq = 0;
+    int64_t bin_count[kNumBins] = {0};
+    int64_t block_entries = 0;      // total local sampled ids
+    bool sampled = false;
+    bool averaging = false;
+    size_t off[40] = {0};
+    size_t total = 0;
+};
+
+enum Slot {
+    O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEG, O_Y0, O_Y0BAR, O_WARM, O_R, O_C, O_TAU, O_ETA, O_G,
+    O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BINIDS, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
+    O_COUNTS, O_NSLOTS
+};
+
+void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
+    pl.m = in->num_segments;
+    pl.N = in->num_products;
+    pl.nq = 0;
+    for (int64_t i = 0; i < pl.m; ++i) {
+        int64_t k = in->seg_ptr[i + 1] - in->seg_ptr[i];
+        int64_t q = (k + 3) / 4;
+        pl.nq += q;
+        int b = bin_of(q);
+        if (b >= 0) pl.bin_count[b] += 1;
+    }
+    pl.sampled = p && p->blocks != nullptr;
+    pl.averaging = p && p->averaging;
+    pl.block_entries = pl.sampled ? p->block_iters * p->block_size : 0;
+    const int64_t nq = std::max<int64_t>(pl.nq, 1), m = std::max<int64_t>(pl.m, 1), N1 = pl.N + 1;
+    size_t sz[O_NSLOTS] = {0};
+    sz[O_PIDX] = nq * 16;
+    sz[O_V] = sz[O_OM] = sz[O_Y] = nq * 32;
+    sz[O_YBAR] = pl.averaging ? nq * 32 : 0;
+    sz[O_QOFF] = (m + 1) * 4;
+    sz[O_SEG] = m * 16;
+    sz[O_Y0] = m * 8;
+    sz[O_Y0BAR] = pl.averaging ? m * 8 : 0;
+    sz[O_WARM] = m * 32;
+    sz[O_R] = sz[O_C] = sz[O_TAU] = sz[O_ETA] = sz[O_G] = sz[O_ACC] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
+    sz[O_ETABAR] = pl.averaging ? N1 * 8 : 0;
+    sz[O_BINIDS] = m * 4;
+    sz[O_BLKIDS] = std::max<int64_t>(pl.block_entries, 1) * 4;
+    sz[O_ROWOFF] = pl.sampled ? p->block_iters * (kNumBins + 1) * 4 : 4;
+    sz[O_RESSEG] = (size_t)kNumBins * kResidBlocks * 4 * 8;
+    sz[O_RESPROD] = (size_t)kResidBlocks * 8 * 8;
+    sz[O_COUNTERS] = 8 * 8;
+    sz[O_T] = 8;
+    sz[O_COUNTS] = N1 * 8;
+    size_t o = 0;
+    for (int s = 0; s < O_NSLOTS; ++s) {
+        pl.off[s] = o;
+        o += align256(sz[s]);
+    }
+    pl.total = o;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct spfom_handle {
+    Plan pl;
+    spfom_params params;
+    int rank = 0, world = 1;
+    nccl_comm comm = nullptr;
+    cudaStream_t stream = nullptr;
+    char *ws = nullptr;
+    DevState S;
+    int64_t nq = 0, m = 0, N = 0, nnz = 0, n_present = 0;
+    std::vector<int32_t> new2old, old2new;     // products
+    std::vector<int64_t> pos_map;              // original entry -> padded entry
+    std::vector<int32_t> bin_first;            // [kNumBins+1] offsets into bin ids
+    int64_t iter = 0;
+    cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
+    std::string err;
+    int sm_count = 148;
+    bool own_stream = false;
+};
+
+namespace {
+spfom_status fail(spfom_handle *h, spfom_status st, const std::string &msg) {
+    if (h) h->err = msg; else g_create_error = msg;
+    return st;
+}
+#define CUDA_TRY(h, expr)                                                                          \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(h, SPFOM_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_));          \
+    } while (0)
+
+template <typename T>
+T *slot_ptr(spfom_handle *h, int s) { return reinterpret_cast<T *>(h->ws + h->pl.off[s]); }
+
+spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, int dtype, int op) {
+    if (h->world <= 1) {
+        if (src != dst) CUDA_TRY(h, cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, h->stream));
+        return SPFOM_OK;
+    }
+    nccl_res r = nccl().AllReduce(src, dst, n, dtype, op, h->comm, h->stream);
+    if (r != 0) return fail(h, SPFOM_ENCCL, std::string("ncclAllReduce: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
+    return SPFOM_OK;
+}
+
+template <int G, int Q, bool ARGMAX>
+void launch_primal(const DevState &S, const SegList &L, int64_t max_count, int sm_count, cudaStream_t st) {
+    const int64_t groups_per_block = kThreads / G;
+    int64_t blocks = (max_count + groups_per_block - 1) / groups_per_block;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count * 64));
+    k_primal<G, Q, ARGMAX><<<(unsigned)blocks, kThreads, 0, st>>>(S, L);
+}
+
+void primal_dispatch(int b, bool argmax, const DevState &S, const SegList &L, int64_t cnt, int sms, cudaStream_t st) {
+    switch (b) {
+#define CASE(B, G, Q)                                                              \
+    case B:                                                                        \
+        if (argmax) launch_primal<G, Q, true>(S, L, cnt, sms, st);                 \
+        else launch_primal<G, Q, false>(S, L, cnt, sms, st);                       \
+        break;
+        CASE(0, 4, 1) CASE(1, 4, 2) CASE(2, 8, 2) CASE(3, 16, 2) CASE(4, 32, 2) CASE(5, 32, 4) CASE(6, 32, 8)
+#undef CASE
+    }
+}
+
+void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, cudaStream_t st) {
+    switch (b) {
+#define CASE(B, G, Q) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part); break;
+        CASE(0, 4, 1) CASE(1, 4, 2) CASE(2, 8, 2) CASE(3, 16, 2) CASE(4, 32, 2) CASE(5, 32, 4) CASE(6, 32, 8)
+#undef CASE
+    }
+}
+
+// Enqueue one iteration (used under stream capture).  refresh: sampled-mode
+// fresh recompute of s = A y before the dual step.
+// a1-a5: the primal kernels, one launch per non-empty length bin
+spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
+    const bool argmax = std::isinf(h->params.theta);
+    DevState S = h->S;
+    int64_t nl = 0;
+    for (int b = 0; b < kNumBins; ++b) {
+        SegList L{};
+        L.bin = b;
+        L.nbins = kNumBins;
+        int64_t maxc = 0;
+        if (h->pl.sampled) {
+            L.ids = slot_ptr<int32_t>(h, O_BLKIDS);
+            L.row_off = slot_ptr<int32_t>(h, O_ROWOFF);
+            L.block_iters = h->params.block_iters;
+            maxc = h->pl.bin_count[b] > 0 ? std::min<int64_t>(h->pl.bin_count[b], h->params.block_size) : 0;
+        } else {
+            const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];
+            bool contiguous = (cnt == h->m);                    // one bin holds every segment: identity list
+            L.ids = contiguous ? nullptr : slot_ptr<int32_t>(h, O_BINIDS);
+            L.first = contiguous ? 0 : h->bin_first[b];
+            L.count = cnt;
+            maxc = cnt;
+        }
+        if (maxc == 0) continue;
+        primal_dispatch(b, argmax, S, L, maxc, h->sm_count, h->stream);
+        ++nl;
+    }
+    CUDA_TRY(h, cudaGetLastError());
+    if (launches) *launches = nl;
+    return SPFOM_OK;
+}
+
+// a6-a8: allreduce of the usage accumulator, dual step, averaging, tick
+spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
+    DevState S = h->S;
+    int64_t nl = 0;
+    double *acc = slot_ptr<double>(h, O_ACC);
+    int full_mode = h->pl.sampled ? 0 : 1;
+    if (refresh) {
+        CUDA_TRY(h, cudaMemsetAsync(acc, 0, (h->N + 1) * 8, h->stream));
+        k_usage<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq, acc);
+        full_mode = 1;
+        ++nl;
+    }
+    spfom_status st = allreduce(h, acc, acc, (size_t)h->N, kNcclFloat64, kNcclSum);
+    if (st != SPFOM_OK) return st;
+    // K3: s_new = full ? acc : s_cur + acc
+    k_dual<<<std::max<int64_t>(1, std::min<int64_t>((h->N + kThreads - 1) / kThreads, h->sm_count * 8)), kThreads, 0,
+             h->stream>>>(S, full_mode);
+    if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq);
+    k_tick<<<1, 1, 0, h->stream>>>(S.t);
+    nl += 2 + (h->pl.averaging ? 1 : 0);
+    CUDA_TRY(h, cudaGetLastError());
+    if (launches) *launches = nl;
+    return SPFOM_OK;
+}
+
+spfom_status enqueue_iteration(spfom_handle *h, bool refresh) {
+    spfom_status st = enqueue_primal(h, nullptr);
+    return st != SPFOM_OK ? st : enqueue_rest(h, refresh, nullptr);
+}
+
+spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out) {
+    cudaGraph_t g;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    spfom_status st = enqueue_iteration(h, refresh);
+    cudaGraph_t gg;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &gg);
+    if (st != SPFOM_OK) return st;
+    if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    g = gg;
+    e = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return SPFOM_OK;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ API
+extern "C" {
+
+const char *spfom_build_info(void) {
+    return "spfom-b200 0.1 (sm_100a, fp64)";
+}
+
+spfom_status spfom_partition(const int64_t *seg_ptr, int64_t m, int32_t world, int64_t *bounds) {
+    if (!seg_ptr || !bounds || world < 1 || m < 0) return SPFOM_EINVAL;
+    const int64_t nnz = seg_ptr[m];
+    bounds[0] = 0;
+    for (int r = 1; r < world; ++r) {
+        // first segment boundary at or after the ideal nnz split
+        const int64_t target = (nnz * r + world - 1) / world;
+        const int64_t *p = std::lower_bound(seg_ptr, seg_ptr + m + 1, target);
+        int64_t b = (int64_t)(p - seg_ptr);
+        // choose the closer of b-1 and b
+        if (b > 0 && b <= m && (target - seg_ptr[b - 1]) < (seg_ptr[b] - target)) b -= 1;
+        b = std::max(b, bounds[r - 1]);
+        bounds[r] = std::min<int64_t>(b, m);
+    }
+    bounds[world] = m;
+    return SPFOM_OK;
+}
+
+spfom_status spfom_nccl_unique_id(void *out128) {
+    if (!out128) return SPFOM_EINVAL;
+    if (!nccl().ok) { g_create_error = "libnccl.so.2 not found"; return SPFOM_ENCCL; }
+    nccl_uid id;
+    if (nccl().GetUniqueId(&id) != 0) { g_create_error = "ncclGetUniqueId failed"; return SPFOM_ENCCL; }
+    memcpy(out128, &id, 128);
+    return SPFOM_OK;
+}
+
+spfom_status spfom_workspace_bytes(const spfom_instance *inst, const spfom_params *params, size_t *bytes) {
+    if (!inst || !bytes || !inst->seg_ptr || inst->num_segments < 0 || inst->num_products < 1)
+        return fail(nullptr, SPFOM_EINVAL, "spfom_workspace_bytes: bad arguments");
+    Plan pl;
+    make_plan(inst, params, pl);
+    *bytes = pl.total;
+    return SPFOM_OK;
+}
+
+static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
+    char buf[256];
+    const int64_t m = in->num_segments, N = in->num_products;
+    if (m < 0 || N < 1 || in->nnz < 0 || !in->seg_ptr || (in->nnz > 0 && (!in->prod_idx || !in->attract)) ||
+        (m > 0 && (!in->no_purchase || !in->arrival)) || !in->price || !in->capacity)
+        return fail(nullptr, SPFOM_EINVAL, "instance: missing array or bad size");
+    if (in->seg_ptr[0] != 0 || in->seg_ptr[m] != in->nnz)
+        return fail(nullptr, SPFOM_EDATA, "instance: seg_ptr[0] must be 0 and seg_ptr[m] == nnz");
+    if (N >= INT32_MAX) return fail(nullptr, SPFOM_EDATA, "instance: num_products too large");
+    for (int64_t i = 0; i < m; ++i) {
+        const int64_t a = in->seg_ptr[i], b = in->seg_ptr[i + 1];
+        if (b < a) { snprintf(buf, sizeof buf, "seg_ptr not monotone at segment %lld", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
+        if ((b - a + 3) / 4 > kMaxQuads) {
+            snprintf(buf, sizeof buf, "segment %lld: consideration set of %lld > 1024 products unsupported", (long long)i, (long long)(b - a));
+            return fail(nullptr, SPFOM_EDATA, buf);
+        }
+        if (!(in->no_purchase[i] > 0.0) || !std::isfinite(in->no_purchase[i])) { snprintf(buf, sizeof buf, "no_purchase[%lld] must be > 0", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
+        if (!(in->arrival[i] > 0.0) || !std::isfinite(in->arrival[i])) { snprintf(buf, sizeof buf, "arrival[%lld] must be > 0", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
+        for (int64_t e = a; e < b; ++e) {
+            const int32_t j = in->prod_idx[e];
+            if (j < 0 || j >= N || (e > a && j <= in->prod_idx[e - 1])) {
+                snprintf(buf, sizeof buf, "prod_idx[%lld] out of range or not strictly increasing in segment %lld", (long long)e, (long long)i);
+                return fail(nullptr, SPFOM_EDATA, buf);
+            }
+            const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
+            if (!(v > 0.0) || !std::isfinite(v) || !(w >= 0.0) || !(w < v)) {
+                snprintf(buf, sizeof buf, "entry %lld: need v > 0 and 0 <= w < v", (long long)e);
+                return fail(nullptr, SPFOM_EDATA, buf);
+            }
+        }
+    }
+    for (int64_t j = 0; j < N; ++j) {
+        if (!(in->price[j] >= 0.0) || !std::isfinite(in->price[j])) { snprintf(buf, sizeof buf, "price[%lld] must be >= 0", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
+        if (!(in->capacity[j] >= 0.0) || !std::isfinite(in->capacity[j])) { snprintf(buf, sizeof buf, "capacity[%lld] must be >= 0", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
+    }
+    if (!p) return fail(nullptr, SPFOM_EINVAL, "params: NULL");
+    if (!(p->theta > 0.0)) return fail(nullptr, SPFOM_EINVAL, "params: theta must be > 0 (INFINITY = exact argmax)");
+    if (!(p->tau > 0.0) || !std::isfinite(p->tau)) return fail(nullptr, SPFOM_EINVAL, "params: tau must be > 0");
+    if (!(p->mu >= 0.0) || !std::isfinite(p->mu)) return fail(nullptr, SPFOM_EINVAL, "params: mu must be >= 0");
+    if (p->tau_mode == 0 && p->tau * p->mu > 1.0) return fail(nullptr, SPFOM_EINVAL, "params: tau * mu must be <= 1 (S:L296)");
+    if (!(p->extrapolation >= 0.0 && p->extrapolation <= 1.0)) return fail(nullptr, SPFOM_EINVAL, "params: extrapolation in [0, 1]");
+    if (p->tau_mode != 0 && p->tau_mode != 1) return fail(nullptr, SPFOM_EINVAL, "params: tau_mode must be 0 or 1");
+    if (p->blocks) {
+        if (p->block_size < 1 || p->block_iters < 1) return fail(nullptr, SPFOM_EINVAL, "params: block_size and block_iters must be >= 1");
+        const int64_t M = in->num_segments_global > 0 ? in->num_segments_global : m;
+        for (int64_t t = 0; t < p->block_iters; ++t) {
+            const int32_t *row = p->blocks + t * p->block_size;
+            for (int64_t b = 0; b < p->block_size; ++b)
+                if (row[b] < 0 || row[b] >= M || (b > 0 && row[b] <= row[b - 1]))
+                    return fail(nullptr, SPFOM_EINVAL, "params: block rows must hold strictly increasing global ids < m");
+        }
+    }
+    return SPFOM_OK;
+}
+
+spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const spfom_dist *dist,
+                          void *cuda_stream, void *workspace, size_t ws_bytes, spfom_handle **out) {
+    if (!in || !out) return fail(nullptr, SPFOM_EINVAL, "spfom_create: NULL argument");
+    *out = nullptr;
+    spfom_status st = validate(in, p);
+    if (st != SPFOM_OK) return st;
+    Plan pl;
+    make_plan(in, p, pl);
+    if (!workspace || ws_bytes < pl.total) return fail(nullptr, SPFOM_ENOMEM, "workspace smaller than spfom_workspace_bytes()");
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0) return fail(nullptr, SPFOM_EINVAL, "workspace must be 256-byte aligned");
+
+    auto *h = new spfom_handle();
+    h->pl = pl;
+    h->params = *p;
+    if (h->params.max_newton <= 0) h->params.max_newton = 64;
+    h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    if (h->stream == nullptr || h->stream == cudaStreamLegacy) {
+        // the legacy default stream cannot be captured into a CUDA graph: use a private one
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            g_create_error = "cudaStreamCreate failed";
+            delete h;
+            return SPFOM_ECUDA;
+        }
+        h->own_stream = true;
+    }
+    h->ws = reinterpret_cast<char *>(workspace);
+    h->m = in->num_segments;
+    h->N = in->num_products;
+    h->nnz = in->nnz;
+    h->nq = pl.nq;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    auto bail = [&](spfom_status s) {
+        g_create_error = h->err;
+        if (h->own_stream) cudaStreamDestroy(h->stream);
+        delete h;
+        return s;
+    };
+
+    if (dist && dist->world > 1) {
+        if (!nccl().ok) { h->err = "world > 1 but libnccl.so.2 not loadable"; return bail(SPFOM_ENCCL); }
+        if (!dist->nccl_id || dist->rank < 0 || dist->rank >= dist->world) { h->err = "bad spfom_dist"; return bail(SPFOM_EINVAL); }
+        h->rank = dist->rank;
+        h->world = dist->world;
+        nccl_uid id;
+        memcpy(&id, dist->nccl_id, 128);
+        if (nccl().CommInitRank(&h->comm, h->world, id, h->rank) != 0) { h->err = "ncclCommInitRank failed"; return bail(SPFOM_ENCCL); }
+    }
+    const int64_t m = h->m, N = h->N;
+
+    // ---- global column counts n_j
+    std::vector<int64_t> counts(N + 1, 0);
+    for (int64_t e = 0; e < in->nnz; ++e) counts[in->prod_idx[e]] += 1;
+    if (h->world > 1) {
+        int64_t *dcounts = slot_ptr<int64_t>(h, O_COUNTS);
+        if (cudaMemcpyAsync(dcounts, counts.data(), N * 8, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D counts"; return bail(SPFOM_ECUDA); }
+        if (allreduce(h, dcounts, dcounts, N, kNcclInt64, kNcclSum) != SPFOM_OK) return bail(SPFOM_ENCCL);
+        if (cudaMemcpyAsync(counts.data(), dcounts, N * 8, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+            cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "D2H counts"; return bail(SPFOM_ECUDA); }
+    }
+    // ---- popularity relabelling: new id = rank by (-n_j, j)
+    h->new2old.resize(N);
+    std::iota(h->new2old.begin(), h->new2old.end(), 0);
+    std::stable_sort(h->new2old.begin(), h->new2old.end(), [&](int32_t a, int32_t b) { return counts[a] > counts[b]; });
+    h->old2new.resize(N);
+    for (int64_t j = 0; j < N; ++j) h->old2new[h->new2old[j]] = (int32_t)j;
+    h->n_present = 0;
+    for (int64_t j = 0; j < N; ++j) h->n_present += counts[j] > 0;
+
+    // ---- per-product arrays (relabelled), slot N = dummy
+    std::vector<double> r(N + 1, 0.0), c(N + 1, 0.0), tau(N + 1, 0.0);
+    for (int64_t jn = 0; jn < N; ++jn) {
+        const int32_t jo = h->new2old[jn];
+        r[jn] = in->price[jo];
+        c[jn] = in->capacity[jo];
+        tau[jn] = (p->tau_mode == 1 && counts[jo] > 0) ? p->tau / (double)counts[jo] : p->tau;
+        if (p->tau_mode == 1 && tau[jn] * p->mu > 1.0) { h->err = "params: tau_j * mu must be <= 1"; return bail(SPFOM_EINVAL); }
+    }
+
+    // ---- padded quad CSR
+    std::vector<int32_t> qoff(m + 1, 0);
+    for (int64_t i = 0; i < m; ++i) qoff[i + 1] = qoff[i] + (int32_t)((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
+    const int64_t nq = qoff[m];
+    std::vector<int32_t> pidx(4 * std::max<int64_t>(nq, 1), (int32_t)N);
+    std::vector<double> vv(4 * std::max<int64_t>(nq, 1), 0.0), om(4 * std::max<int64_t>(nq, 1), 0.0);
+    std::vector<double2> seg(std::max<int64_t>(m, 1));
+    std::vector<double4> warm(std::max<int64_t>(m, 1));
+    h->pos_map.assign(in->nnz, 0);
+    bool bad_numeric = false;
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t i = 0; i < m; ++i) {
+        const int64_t a = in->seg_ptr[i], k = in->seg_ptr[i + 1] - a;
+        std::vector<std::pair<int32_t, int64_t>> order(k);
+        for (int64_t q = 0; q < k; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
+        std::sort(order.begin(), order.end());
+        double vt0 = in->no_purchase[i], svt = 0.0;
+        const int64_t base = 4 * (int64_t)qoff[i];
+        for (int64_t q = 0; q < k; ++q) {
+            const int64_t e = order[q].second;
+            const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
+            pidx[base + q] = order[q].first;
+            vv[base + q] = v;
+            om[base + q] = w / v;
+            vt0 += w;
+            svt += v - w;
+            h->pos_map[e] = base + q;
+        }
+        seg[i] = make_double2(in->arrival[i], vt0);
+        // initial projection multipliers (nu, kappa, U)
+        warm[i] = make_double4(0.0, 0.0, in->arrival[i] / (vt0 + svt), 0.0);
+        if (!std::isfinite(vt0)) bad_numeric = true;
+    }
+    if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
+
+    // ---- bins (full sweep lists) and sampled block tables
+    h->bin_first.assign(kNumBins + 1, 0);
+    std::vector<int32_t> binids(std::max<int64_t>(m, 1));
+    {
+        std::vector<int64_t> cnt(kNumBins, 0);
+        std::vector<int> segbin(m);
+        for (int64_t i = 0; i < m; ++i) { segbin[i] = bin_of(qoff[i + 1] - qoff[i]); cnt[segbin[i]]++; }
+        for (int b = 0; b < kNumBins; ++b) h->bin_first[b + 1] = (int32_t)(h->bin_first[b] + cnt[b]);
+        std::vector<int64_t> fill(h->bin_first.begin(), h->bin_first.end() - 1);
+        for (int64_t i = 0; i < m; ++i) binids[fill[segbin[i]]++] = (int32_t)i;
+        std::vector<int32_t> rowoff;
+        std::vector<int32_t> blkids;
+        if (pl.sampled) {
+            const int64_t off = in->segment_offset;
+            rowoff.assign(p->block_iters * (kNumBins + 1), 0);
+            std::vector<std::vector<int32_t>> per(kNumBins);
+            for (int64_t t = 0; t < p->block_iters; ++t) {
+                for (auto &v : per) v.clear();
+                const int32_t *row = p->blocks + t * p->block_size;
+                for (int64_t b = 0; b < p->block_size; ++b) {
+                    const int64_t li = (int64_t)row[b] - off;
+                    if (li >= 0 && li < m) per[segbin[li]].push_back((int32_t)li);
+                }
+                int32_t *ro = rowoff.data() + t * (kNumBins + 1);
+                ro[0] = (int32_t)blkids.size();
+                for (int b = 0; b < kNumBins; ++b) {
+                    blkids.insert(blkids.end(), per[b].begin(), per[b].end());
+                    ro[b + 1] = (int32_t)blkids.size();
+                }
+            }
+            // per-bin max count per row, for static grid sizes
+            for (int b = 0; b < kNumBins; ++b) {
+                int64_t mx = 0;
+                for (int64_t t = 0; t < p->block_iters; ++t) {
+                    const int32_t *ro = rowoff.data() + t * (kNumBins + 1);
+                    mx = std::max<int64_t>(mx, ro[b + 1] - ro[b]);
+                }
+                h->pl.bin_count[b] = mx;
+            }
+            if (!blkids.empty() && cudaMemcpyAsync(slot_ptr<int32_t>(h, O_BLKIDS), blkids.data(), blkids.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D blocks"; return bail(SPFOM_ECUDA); }
+            if (cudaMemcpyAsync(slot_ptr<int32_t>(h, O_ROWOFF), rowoff.data(), rowoff.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D rowoff"; return bail(SPFOM_ECUDA); }
+            if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "sync"; return bail(SPFOM_ECUDA); }
+        }
+    }
+
+    // ---- copies into the workspace
+    auto H2D = [&](int slot, const void *src, size_t bytes) {
+        return bytes == 0 || cudaMemcpyAsync(h->ws + h->pl.off[slot], src, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
+    };
+    std::vector<double> y0(std::max<int64_t>(m, 1));
+    for (int64_t i = 0; i < m; ++i) y0[i] = in->arrival[i];
+    bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
+              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEG, seg.data(), m * 16) && H2D(O_Y0, y0.data(), m * 8) &&
+              H2D(O_WARM, warm.data(), m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
+              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8) && H2D(O_BINIDS, binids.data(), m * 4);
+    if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), m * 8);
+    auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
+    ok = ok && Z(O_Y, nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (N + 1) * 8) && Z(O_SCUR, (N + 1) * 8) &&
+         Z(O_COUNTERS, 64) && Z(O_T, 8);
+    if (pl.averaging) ok = ok && Z(O_YBAR, nq * 32) && Z(O_ETABAR, (N + 1) * 8);
+    if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
+
+    DevState &S = h->S;
+    S.pidx = slot_ptr<int4>(h, O_PIDX);
+    S.v = slot_ptr<double>(h, O_V);
+    S.om = slot_ptr<double>(h, O_OM);
+    S.y = slot_ptr<double>(h, O_Y);
+    S.ybar = pl.averaging ? slot_ptr<double>(h, O_YBAR) : nullptr;
+    S.qoff = slot_ptr<int32_t>(h, O_QOFF);
+    S.seg = slot_ptr<double2>(h, O_SEG);
+    S.y0 = slot_ptr<double>(h, O_Y0);
+    S.y0bar = pl.averaging ? slot_ptr<double>(h, O_Y0BAR) : nullptr;
+    S.warm = slot_ptr<double4>(h, O_WARM);
+    S.r = slot_ptr<double>(h, O_R);
+    S.c = slot_ptr<double>(h, O_C);
+    S.tau = slot_ptr<double>(h, O_TAU);
+    S.eta = slot_ptr<double>(h, O_ETA);
+    S.g = slot_ptr<double>(h, O_G);
+    S.s = slot_ptr<double>(h, O_ACC);
+    S.s_prev = slot_ptr<double>(h, O_SCUR);
+    S.etabar = pl.averaging ? slot_ptr<double>(h, O_ETABAR) : nullptr;
+    S.counters = slot_ptr<unsigned long long>(h, O_COUNTERS);
+    S.t = slot_ptr<int64_t>(h, O_T);
+    S.m = m;
+    S.N = N;
+    S.theta = p->theta;
+    S.mu = p->mu;
+    S.omega_x = p->extrapolation;
+    S.max_newton = h->params.max_newton;
+    S.sampled = pl.sampled ? 1 : 0;
+
+    st = build_graph(h, false, &h->graph);
+    if (st != SPFOM_OK) return bail(st);
+    if (pl.sampled && p->refresh_every > 0) {
+        st = build_graph(h, true, &h->graph_refresh);
+        if (st != SPFOM_OK) return bail(st);
+    }
+    *out = h;
+    return SPFOM_OK;
+}
+
+spfom_status spfom_step(spfom_handle *h, int64_t k) {
+    if (!h || k < 0) return SPFOM_EINVAL;
+    for (int64_t it = 0; it < k; ++it) {
+        const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
+        CUDA_TRY(h, cudaGraphLaunch(refresh ? h->graph_refresh : h->graph, h->stream));
+        h->iter += 1;
+    }
+    return SPFOM_OK;
+}
+
+static spfom_status check_counters(spfom_handle *h) {
+    unsigned long long cnt[3];
+    CUDA_TRY(h, cudaMemcpyAsync(cnt, h->S.counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (cnt[0] != 0) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "projection hit max_newton on %llu segment-iterations", cnt[0]);
+        h->err = buf;
+        return SPFOM_ENUMERIC;
+    }
+    return SPFOM_OK;
+}
+
+spfom_status spfom_duals(spfom_handle *h, double *eta) {
+    if (!h || !eta) return SPFOM_EINVAL;
+    std::vector<double> tmp(h->N);
+    CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.eta, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (int64_t jn = 0; jn < h->N; ++jn) eta[h->new2old[jn]] = tmp[jn];
+    return check_counters(h);
+}
+
+spfom_status spfom_usage(spfom_handle *h, double *s) {
+    if (!h || !s) return SPFOM_EINVAL;
+    std::vector<double> tmp(h->N);
+    CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.s_prev, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    for (int64_t jn = 0; jn < h->N; ++jn) s[h->new2old[jn]] = tmp[jn];
+    return SPFOM_OK;
+}
+
+static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, double *y, double *y0) {
+    std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1));
+    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), dy, h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
+    if (y0 && h->m) CUDA_TRY(h, cudaMemcpyAsync(y0, dy0, h->m * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (y)
+        for (int64_t e = 0; e < h->nnz; ++e) y[e] = tmp[h->pos_map[e]];
+    return SPFOM_OK;
+}
+
+spfom_status spfom_primal(spfom_handle *h, double *y, double *y0) {
+    if (!h) return SPFOM_EINVAL;
+    spfom_status st = fetch_primal(h, h->S.y, h->S.y0, y, y0);
+    return st != SPFOM_OK ? st : check_counters(h);
+}
+
+spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double *etabar) {
+    if (!h) return SPFOM_EINVAL;
+    if (!h->pl.averaging) return fail(h, SPFOM_EINVAL, "averaging is off");
+    spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, ybar, y0bar);
+    if (st != SPFOM_OK) return st;
+    if (etabar) {
+        std::vector<double> tmp(h->N);
+        CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.etabar, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        for (int64_t jn = 0; jn < h->N; ++jn) etabar[h->new2old[jn]] = tmp[jn];
+    }
+    return SPFOM_OK;
+}
+
+spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
+    if (!h || !out) return SPFOM_EINVAL;
+    DevState S = h->S;
+    double *sf = slot_ptr<double>(h, O_TMP);
+    CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));
+    k_usage<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq, sf);
+    spfom_status st = allreduce(h, sf, sf, (size_t)h->N, kNcclFloat64, kNcclSum);
+    if (st != SPFOM_OK) return st;
+    double *pseg = slot_ptr<double>(h, O_RESSEG);
+    CUDA_TRY(h, cudaMemsetAsync(pseg, 0, (size_t)kNumBins * kResidBlocks * 4 * 8, h->stream));
+    for (int b = 0; b < kNumBins; ++b) {
+        const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];
+        if (cnt == 0) continue;
+        SegList L{};
+        L.ids = slot_ptr<int32_t>(h, O_BINIDS);
+        L.first = h->bin_first[b];
+        L.count = cnt;
+        resid_dispatch(b, S, L, pseg + (size_t)b * kResidBlocks * 4, h->stream);
+    }
+    double *pprod = slot_ptr<double>(h, O_RESPROD);
+    k_resid_prod<<<kResidBlocks, kThreads, 0, h->stream>>>(S, sf, h->n_present, pprod);
+    CUDA_TRY(h, cudaGetLastError());
+    // cross-rank: sum of D_seg, max of the audits (local segment quantities)
+    double *red = slot_ptr<double>(h, O_COUNTS);   // reuse the counts slot as scratch (>= 4 doubles)
+    std::vector<double> hs((size_t)kNumBins * kResidBlocks * 4), hp((size_t)kResidBlocks * 8);
+    CUDA_TRY(h, cudaMemcpyAsync(hs.data(), pseg, hs.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(hp.data(), pprod, hp.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    unsigned long long cnt[3];
+    CUDA_TRY(h, cudaMemcpyAsync(cnt, h->S.counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    double dseg = 0.0, agg[3] = {0, 0, 0};
+    for (size_t bb = 0; bb < (size_t)kNumBins * kResidBlocks; ++bb) {
+        dseg += hs[4 * bb];
+        for (int k = 0; k < 3; ++k) agg[k] = std::max(agg[k], hs[4 * bb + 1 + k]);
+    }
+    double pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < kResidBlocks; ++b)
+        for (int k = 0; k < 8; ++k)
+            pr[k] = (k == 2 || k == 3 || k == 7) ? std::max(pr[k], hp[8 * b + k]) : pr[k] + hp[8 * b + k];
+    if (h->world > 1) {
+        double buf[4] = {dseg, agg[0], agg[1], agg[2]};
+        CUDA_TRY(h, cudaMemcpyAsync(red, buf, 32, cudaMemcpyHostToDevice, h->stream));
+        if ((st = allreduce(h, red, red, 1, kNcclFloat64, kNcclSum)) != SPFOM_OK) return st;
+        if ((st = allreduce(h, red + 1, red + 1, 3, kNcclFloat64, kNcclMax)) != SPFOM_OK) return st;
+        CUDA_TRY(h, cudaMemcpyAsync(buf, red, 32, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        dseg = buf[0];
+        agg[0] = buf[1]; agg[1] = buf[2]; agg[2] = buf[3];
+    }
+    const double P = pr[0], D = pr[1] + dseg;
+    out->iteration = h->iter;
+    out->primal_obj = P;
+    out->dual_obj = D;
+    out->rel_gap = (D - P) / (1.0 + std::fabs(P) + std::fabs(D));
+    out->infeas_abs = pr[2];
+    out->infeas_rel = pr[3];
+    out->infeas_rel_l2 = std::sqrt(pr[4]) / (1.0 + std::sqrt(pr[5]));
+    out->balance_rel_max = agg[0];
+    out->scale_rel_max = agg[1];
+    out->neg_max = agg[2];
+    out->compl_slack = pr[6] / (1.0 + std::fabs(P));
+    out->alpha = pr[7];
+    out->cert_lower = (1.0 - pr[7]) * P;
+    out->cert_upper = D;
+    out->newton_failures = (int64_t)cnt[0];
+    out->newton_passes = (int64_t)cnt[1];
+    return SPFOM_OK;
+}
+
+spfom_status spfom_objective(spfom_handle *h, double *obj) {
+    if (!h || !obj) return SPFOM_EINVAL;
+    spfom_residuals_t r;
+    spfom_status st = spfom_residuals(h, &r);
+    if (st == SPFOM_OK) *obj = r.primal_obj;
+    return st;
+}
+
+spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0, const double *eta, const double *s_prev) {
+    if (!h) return SPFOM_EINVAL;
+    if (y) {
+        std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1), 0.0);
+        for (int64_t e = 0; e < h->nnz; ++e) tmp[h->pos_map[e]] = y[e];
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.y, tmp.data(), h->nq * 32, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    }
+    if (y0) CUDA_TRY(h, cudaMemcpyAsync(h->S.y0, y0, h->m * 8, cudaMemcpyHostToDevice, h->stream));
+    std::vector<double> t1(h->N + 1, 0.0), t2(h->N + 1, 0.0);
+    if (eta) {
+        std::vector<double> r(h->N + 1, 0.0);
+        CUDA_TRY(h, cudaMemcpyAsync(r.data(), h->S.r, (h->N + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        for (int64_t jn = 0; jn < h->N; ++jn) { t1[jn] = eta[h->new2old[jn]]; t2[jn] = r[jn] - t1[jn]; }
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.eta, t1.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.g, t2.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    }
+    if (s_prev) {
+        std::vector<double> t3(h->N + 1, 0.0);
+        for (int64_t jn = 0; jn < h->N; ++jn) t3[jn] = s_prev[h->new2old[jn]];
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.s_prev, t3.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return SPFOM_OK;
+}
+
+spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
+    if (!h_ || !out) return SPFOM_EINVAL;
+    spfom_handle *h = const_cast<spfom_handle *>(h_);
+    memset(out, 0, sizeof *out);
+    out->num_segments = h->m;
+    out->num_products = h->N;
+    out->nnz = h->nnz;
+    out->nnz_padded = 4 * h->nq;
+    out->n_present = h->n_present;
+    out->workspace_bytes = (int64_t)h->pl.total;
+    out->num_bins = kNumBins;
+    out->world = h->world;
+    int64_t np = 0;
+    for (int b = 0; b < kNumBins; ++b) {
+        out->bin_G[b] = kBins[b].G;
+        out->bin_Q[b] = kBins[b].Q;
+        out->bin_segments[b] = h->pl.sampled ? h->pl.bin_count[b] : (h->bin_first[b + 1] - h->bin_first[b]);
+        np += out->bin_segments[b] > 0;
+    }
+    out->primal_launches_per_iteration = np;
+    out->launches_per_iteration = np + 2 + (h->pl.averaging ? 1 : 0);
+    return SPFOM_OK;
+}
+
+spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms) {
+    if (!h || !ms || iters < 1) return SPFOM_EINVAL;
+    cudaEvent_t ev[3];
+    for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int64_t it = 0; it < iters; ++it) {
+        const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
+        CUDA_TRY(h, cudaEventRecord(ev[0], h->stream));
+        spfom_status st = enqueue_primal(h, nullptr);
+        if (st != SPFOM_OK) return st;
+        CUDA_TRY(h, cudaEventRecord(ev[1], h->stream));
+        st = enqueue_rest(h, refresh, nullptr);
+        if (st != SPFOM_OK) return st;
+        CUDA_TRY(h, cudaEventRecord(ev[2], h->stream));
+        CUDA_TRY(h, cudaEventSynchronize(ev[2]));
+        float a = 0.f, b = 0.f;
+        CUDA_TRY(h, cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CUDA_TRY(h, cudaEventElapsedTime(&b, ev[1], ev[2]));
+        acc0 += a;
+        acc1 += b;
+        h->iter += 1;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    ms[0] = acc0;
+    ms[1] = acc1;
+    return SPFOM_OK;
+}
+
+int64_t spfom_iteration(const spfom_handle *h) { return h ? h->iter : -1; }
+
+const char *spfom_last_error(const spfom_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void spfom_destroy(spfom_handle *h) {
+    if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->graph) cudaGraphExecDestroy(h->graph);
+    if (h->graph_refresh) cudaGraphExecDestroy(h->graph_refresh);
+    if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (-m gpu).
+
+Tolerances (north_star / SURVEY §8(c) c13): per-iterate rel-inf <= 1e-10 for
+the first 100 iterations; final objective within 1e-6 of the LP optimum;
+primal infeasibility <= 1e-6.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import lp
+from spfom_inputs import Instance, block_sequence, generate
+from tests.parity import TOL_ITER, lockstep, oracle_kwargs, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "lp_optima.json")
+
+
+def _params(**kw):
+    from paper_2602_22421_b200 import Params
+    return Params(**kw)
+
+
+def _paper(**kw):
+    from paper_2602_22421_b200 import Params
+    return Params.paper(**kw)
+
+
+def _assert_ok(worst):
+    assert "first_bad_iter" not in worst and max(worst[k] for k in ("y", "y0", "eta", "s")) <= TOL_ITER, worst
+
+
+# ------------------------------------------------------------ per-iterate parity
+@pytest.mark.parametrize("name,kw", [
+    ("tiny", {}),
+    ("small", {}),
+    ("medium", dict(m=2000, N=1500, k=(20, 200))),          # four length bins, Zipf head
+    ("multi", dict(m=400, N=300, k=50, T=3)),               # stacked periods, shared inventory
+])
+def test_converge_preset_lockstep_100(name, kw):
+    inst = generate(name, **kw)
+    worst, gpu, _ = lockstep(inst, _params(), 100)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def _ragged_instance(ks, N=1100, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = [np.sort(rng.choice(N, k, replace=False)) for k in ks]
+    seg_ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    prod = np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32)
+    nnz = prod.shape[0]
+    v = rng.uniform(0.1, 1.0, nnz)
+    w = v * rng.uniform(0.0, 0.5, nnz)
+    m = len(ks)
+    v0 = rng.uniform(0.5, 2.0, m)
+    lam = rng.uniform(1.0, 10.0, m)
+    r = rng.lognormal(3.0, 0.5, N)
+    cnt = np.bincount(prod, minlength=N)
+    d = np.zeros(N)
+    for i in range(m):
+        sl = slice(seg_ptr[i], seg_ptr[i + 1])
+        d += np.bincount(prod[sl], weights=lam[i] * v[sl] / (v0[i] + v[sl].sum()), minlength=N)
+    c = np.where(cnt > 0, 0.4 * d, 1.0)
+    return Instance("ragged", seg_ptr, prod, v, w, v0, lam, r, c, cnt > 0, {})
+
+
+def test_ragged_lengths_cross_every_bin_and_pad():
+    """Edge cases: k = 0 (empty consideration set), 1, pad widths 1..3, every
+    bin boundary (16/32/64/128/256/512/1024 entries)."""
+    ks = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257,
+          300, 511, 512, 513, 1000, 1024, 0, 6, 50] * 3
+    inst = _ragged_instance(ks)
+    worst, gpu, cpu = lockstep(inst, _params(), 60)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def test_mnl_special_case_lockstep():
+    """omega = 0 (MNL) is the GAM special case."""
+    inst = generate("small", m=500, N=300, k=(10, 80))
+    inst.shadow[:] = 0.0
+    worst, gpu, _ = lockstep(inst, _params(), 60)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def test_theta_variants_lockstep():
+    inst = generate("small", m=600, N=300, k=(10, 70))
+    for theta in (0.05, 0.3, 5.0):
+        worst, gpu, _ = lockstep(inst, _params(theta=theta, tau=0.9 / max(theta, 1.0)), 40)
+        gpu.close()
+        _assert_ok(worst)
+
+
+def test_paper_preset_sampled_lockstep_100():
+    """Alg. 2 literal: theta = inf (exact inner argmax), scalar tau = 0.1,
+    Eq. 17 with mu = 0.5, sampled blocks of B = 100, no extrapolation."""
+    inst = generate("small")
+    blocks = block_sequence(inst.m, 100, 100, seed=7)
+    worst, gpu, cpu = lockstep(inst, _paper(mu=0.5, blocks=blocks), 100, blocks=blocks)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def test_paper_preset_full_sweep_lockstep():
+    inst = generate("small", m=800, N=400, k=(10, 90))
+    worst, gpu, _ = lockstep(inst, _paper(mu=0.0), 100)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def test_sampled_finite_theta_with_refresh():
+    inst = generate("medium", m=1500, N=600, k=(20, 120))
+    blocks = block_sequence(inst.m, 257, 13, seed=3)
+    worst, gpu, _ = lockstep(inst, _params(blocks=blocks, refresh_every=7), 60, blocks=blocks)
+    gpu.close()
+    _assert_ok(worst)
+
+
+def test_averaging_parity():
+    inst = generate("small", m=500, N=250, k=(5, 60))
+    p = _params(averaging=True)
+    worst, gpu, cpu = lockstep(inst, p, 50)
+    _assert_ok(worst)
+    yb, y0b, eb = gpu.averages()
+    gpu.close()
+    lam, rmax = float(inst.arrival.max()), float(inst.price.max())
+    assert rel_inf(yb, cpu.ybar, lam) <= TOL_ITER and rel_inf(y0b, cpu.y0bar, lam) <= TOL_ITER
+    assert rel_inf(eb, cpu.etabar, rmax) <= TOL_ITER
+
+
+def test_residuals_match_oracle():
+    inst = generate("small")
+    worst, gpu, cpu = lockstep(inst, _params(), 50, check_every=50)
+    _assert_ok(worst)
+    rg = gpu.residuals()
+    ro = cpu.residuals()
+    gpu.close()
+    for k in ("primal_obj", "dual_obj", "cert_lower", "cert_upper"):
+        assert abs(rg[k] - ro[k]) <= 1e-10 * abs(ro[k]), (k, rg[k], ro[k])
+    for k in ("infeas_abs", "infeas_rel", "infeas_rel_l2", "alpha", "compl_slack"):
+        assert abs(rg[k] - ro[k]) <= 1e-10 * max(1.0, abs(ro[k])), (k, rg[k], ro[k])
+    assert rg["balance_rel_max"] <= 1e-13 and rg["scale_rel_max"] <= 1e-13 and rg["neg_max"] == 0.0
+    assert rg["newton_failures"] == 0
+
+
+def test_checkpoint_resume():
+    from paper_2602_22421_b200 import Solver
+    inst = generate("small", m=400, N=200, k=(5, 60))
+    a = Solver(inst, _params())
+    a.step(20)
+    y, y0 = a.primal()
+    eta, s = a.duals(), a.usage()
+    b = Solver(inst, _params())
+    b.set_state(y=y, y0=y0, eta=eta, s_prev=s)
+    a.step(10)
+    b.step(10)
+    ya, _ = a.primal()
+    yb, _ = b.primal()
+    assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
+# ------------------------------------------------------------ accuracy gates
+@pytest.mark.parametrize("seed", [1, 11, 12])
+def test_tiny_accuracy_vs_dense_lp(seed):
+    from paper_2602_22421_b200 import Solver
+    inst = generate("tiny", seed=seed)
+    Pstar = lp.sblp_dense(inst)[0]
+    gpu = Solver(inst, _params())
+    gpu.step(2000)
+    r = gpu.residuals()
+    gpu.close()
+    assert abs(r["primal_obj"] - Pstar) <= 1e-6 * Pstar and r["infeas_rel"] <= 1e-6
+
+
+def test_small_accuracy_vs_highs():
+    from paper_2602_22421_b200 import Solver
+    gold = json.load(open(GOLD))["small"]
+    inst = generate("small")
+    gpu = Solver(inst, _params())
+    gpu.step(3000)
+    r = gpu.residuals()
+    gpu.close()
+    assert abs(r["primal_obj"] - gold["Pstar"]) <= 1e-6 * gold["Pstar"], (r, gold)
+    assert r["infeas_rel"] <= 1e-6
+    assert r["cert_lower"] <= gold["Pstar"] * (1 + 1e-9) and gold["Pstar"] <= r["cert_upper"] * (1 + 1e-9)
+
+
+# ------------------------------------------------------------ full-size sampled checks
+def _check_sampled_segments(inst, gpu, eta_prev, y_prev, y0_prev, n_sample=3000, seed=0):
+    """After one iteration from (y_prev, y0_prev, eta_prev), every segment's new
+    row is the oracle projection of its own gradient step -- computable one by one."""
+    rng = np.random.default_rng(seed)
+    y, y0 = gpu.primal()
+    g = inst.price - eta_prev
+    worst = 0.0
+    for i in rng.choice(inst.m, size=min(n_sample, inst.m), replace=False):
+        sl = inst.row(int(i))
+        z = y_prev[sl] + 1.0 * g[inst.prod_idx[sl]]
+        r0, ry, _m, _ = oracle.project(y0_prev[i], z, inst.attract[sl], inst.shadow[sl], inst.no_purchase[i],
+                                       inst.arrival[i])
+        lam = inst.arrival[i]
+        worst = max(worst, abs(y0[i] - r0) / lam, float(np.abs(y[sl] - ry).max()) / lam if ry.size else 0.0)
+    return worst, y, y0
+
+
+@pytest.mark.parametrize("name", ["medium", "huge"])
+def test_full_size_sampled_outputs(name):
+    """BASELINE full sizes in the bench launch configuration: sampled segment
+    rows vs the oracle's projection, the usage vector vs a fresh sum, and eta
+    vs the oracle's Eq. 17 step on that usage."""
+    from paper_2602_22421_b200 import Solver
+    inst = generate(name)
+    gpu = Solver(inst, _params())
+    gpu.step(3)
+    y_prev, y0_prev = gpu.primal()
+    eta_prev, s_prev = gpu.duals(), gpu.usage()
+    gpu.step(1)
+    worst, y, y0 = _check_sampled_segments(inst, gpu, eta_prev, y_prev, y0_prev)
+    assert worst <= 1e-12, worst
+    s = gpu.usage()
+    fresh = np.bincount(inst.prod_idx, weights=y, minlength=inst.N)
+    assert rel_inf(s, fresh, 1.0) <= 1e-12
+    cpu = oracle.OracleSolver(generate("tiny"))       # only for tau_j via the oracle's own rule
+    n = np.bincount(inst.prod_idx, minlength=inst.N)
+    tau_j = np.where(n > 0, 0.9 / np.maximum(n, 1), 0.9)
+    eta_ref = oracle.dual_step(eta_prev, s, s_prev, inst.capacity, tau_j, 0.0, 1.0)
+    assert rel_inf(gpu.duals(), eta_ref, float(inst.price.max())) <= 1e-12
+    r = gpu.residuals()
+    gpu.close()
+    assert r["newton_failures"] == 0 and r["balance_rel_max"] <= 1e-12 and r["neg_max"] == 0.0
+    del cpu
