@@ -40,7 +40,28 @@ def parse_args():
     ap.add_argument("--config", default="huge")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-iters", type=int, default=50)
+    ap.add_argument("--cache", default=None, help="directory to cache the generated instance (npz)")
     return ap.parse_args()
+
+
+def load_instance(name: str, cache):
+    from spfom_inputs import Instance, generate
+
+    if not cache:
+        return generate(name)
+    import numpy as np
+
+    path = os.path.join(cache, f"{name}.npz")
+    if os.path.exists(path):
+        z = np.load(path, allow_pickle=True)
+        return Instance(name, z["seg_ptr"], z["prod_idx"], z["attract"], z["shadow"], z["no_purchase"],
+                        z["arrival"], z["price"], z["capacity"], z["present"], z["meta"].item())
+    inst = generate(name)
+    os.makedirs(cache, exist_ok=True)
+    np.savez(path, seg_ptr=inst.seg_ptr, prod_idx=inst.prod_idx, attract=inst.attract, shadow=inst.shadow,
+             no_purchase=inst.no_purchase, arrival=inst.arrival, price=inst.price, capacity=inst.capacity,
+             present=inst.present, meta=np.array(inst.meta, dtype=object))
+    return inst
 
 
 def measured_peaks():
@@ -150,7 +171,7 @@ def run_reference(args, rank, world):
         return
     from spfom_inputs import generate
 
-    inst = generate(args.config)
+    inst = load_instance(args.config, args.cache)
     # size each step so that warmup + steps finish within ~3 minutes
     budget_per_step = min(1.0, 150.0 / max(1, args.steps + args.warmup))
     import oracle
@@ -216,7 +237,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
 
-    inst = generate(args.config)
+    inst = load_instance(args.config, args.cache)
     bounds = partition(inst.seg_ptr, world)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     shard = inst.segment_slice(lo, hi) if world > 1 else inst
@@ -325,7 +346,8 @@ def main():
                                   "iterations + duals()+primal() D2H, through the C ABI"},
             "gpu_launches": int(info["launches_per_iteration"]) * args.steps,
             "cpu_baseline": cpu_baseline,
-            "residuals_after": {k: res[k] for k in ("iteration", "rel_gap", "infeas_rel", "newton_failures")},
+            "residuals_after": {k: res[k] for k in ("iteration", "rel_gap", "infeas_rel", "newton_failures",
+                                                    "newton_restarts")},
             "newton_passes_per_segment_iteration": res["newton_passes"] / max(1, res["iteration"] * shard.m),
         }
         print(json.dumps(line), flush=True)

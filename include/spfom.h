@@ -107,7 +107,10 @@ typedef struct {
  *                  t uses row t mod block_iters.  Copied at create.
  *   refresh_every  sampled mode: recompute s = A y from scratch every K
  *                  iterations (0 = never)
- *   max_newton     cap on projection passes per segment (0 => 64)
+ *   max_newton     cap on projection passes per segment (0 => 200); a segment
+ *                  still unconverged after half of it restarts from the cold
+ *                  point; one that exhausts it is counted as a failure and
+ *                  makes the next synchronising getter return SPFOM_ENUMERIC
  */
 typedef struct {
     double theta;
@@ -151,6 +154,7 @@ typedef struct {
     double alpha;
     int64_t newton_failures;/* segments whose projection hit max_newton     */
     int64_t newton_passes;  /* total projection passes since create         */
+    int64_t newton_restarts;/* segment-iterations that used the cold restart */
 } spfom_residuals_t;
 
 typedef struct spfom_handle spfom_handle;

@@ -10,7 +10,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libspfom.so")
 SOURCES = [os.path.join(CSRC, "spfom.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "spfom_kernels.cuh"), os.path.join(ROOT, "include", "spfom.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("spfom_kernels.cuh", "spfom_primal.cuh", "spfom_common.cuh")] + [
+    os.path.join(ROOT, "include", "spfom.h")]
 
 
 def nvcc_cmd(out: str = SO, extra=()):

@@ -61,8 +61,12 @@ NcclApi &nccl() {
 thread_local std::string g_create_error;
 
 // Bin = (G lanes per segment, Q quads per lane) -> capacity 4 G Q entries.
+// (G lanes per segment, Q quads per lane); capacities 16 .. 1024 entries.
+#define SPFOM_BINS(X) X(0, 4, 1) X(1, 4, 2) X(2, 8, 2) X(3, 16, 2) X(4, 32, 2) X(5, 32, 4) X(6, 32, 8)
 struct BinCfg { int G, Q; };
-constexpr BinCfg kBins[] = {{4, 1}, {4, 2}, {8, 2}, {16, 2}, {32, 2}, {32, 4}, {32, 8}};
+#define SPFOM_BIN_INIT(B, G, Q) {G, Q},
+constexpr BinCfg kBins[] = {SPFOM_BINS(SPFOM_BIN_INIT)};
+#undef SPFOM_BIN_INIT
 constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
 constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
 
@@ -180,22 +184,40 @@ spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, in
     return SPFOM_OK;
 }
 
-template <int G, int Q, bool ARGMAX>
-void launch_primal(const DevState &S, const SegList &L, int64_t max_count, int sm_count, cudaStream_t st) {
-    const int64_t groups_per_block = kThreads / G;
+// Persistent grid: at most (resident blocks per SM) x SMs blocks, each looping
+// over segments; the Zipf head is privatised only when a block sees enough
+// segments to amortise its flush (H REDs per block).
+template <int G, int Q, bool ARGMAX, bool SAMPLED>
+void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count, cudaStream_t st) {
+    static int resident = 0;
+    constexpr size_t smem = sizeof(PrimalSmem<Q>);
+    if (resident == 0) {
+        cudaFuncSetAttribute(k_primal<G, Q, ARGMAX, SAMPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_primal<G, Q, ARGMAX, SAMPLED>, kPrimalThreads, smem);
+        resident = std::max(resident, 1);
+    }
+    const int64_t groups_per_block = kPrimalThreads / G;
     int64_t blocks = (max_count + groups_per_block - 1) / groups_per_block;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count * 64));
-    k_primal<G, Q, ARGMAX><<<(unsigned)blocks, kThreads, 0, st>>>(S, L);
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count * resident));
+    const int64_t segs_per_block = (max_count + blocks - 1) / blocks;
+    L.head = (segs_per_block >= 64) ? (int32_t)std::min<int64_t>(kHeadMax, S.N) : 0;
+    k_primal<G, Q, ARGMAX, SAMPLED><<<(unsigned)blocks, kPrimalThreads, smem, st>>>(S, L);
 }
 
-void primal_dispatch(int b, bool argmax, const DevState &S, const SegList &L, int64_t cnt, int sms, cudaStream_t st) {
+void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int sms,
+                     cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q)                                                              \
-    case B:                                                                        \
-        if (argmax) launch_primal<G, Q, true>(S, L, cnt, sms, st);                 \
-        else launch_primal<G, Q, false>(S, L, cnt, sms, st);                       \
+#define CASE(B, G, Q)                                                                      \
+    case B:                                                                                \
+        if (argmax) {                                                                      \
+            if (sampled) launch_primal<G, Q, true, true>(S, L, cnt, sms, st);              \
+            else launch_primal<G, Q, true, false>(S, L, cnt, sms, st);                     \
+        } else {                                                                           \
+            if (sampled) launch_primal<G, Q, false, true>(S, L, cnt, sms, st);             \
+            else launch_primal<G, Q, false, false>(S, L, cnt, sms, st);                    \
+        }                                                                                  \
         break;
-        CASE(0, 4, 1) CASE(1, 4, 2) CASE(2, 8, 2) CASE(3, 16, 2) CASE(4, 32, 2) CASE(5, 32, 4) CASE(6, 32, 8)
+        SPFOM_BINS(CASE)
 #undef CASE
     }
 }
@@ -203,7 +225,7 @@ void primal_dispatch(int b, bool argmax, const DevState &S, const SegList &L, in
 void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part); break;
-        CASE(0, 4, 1) CASE(1, 4, 2) CASE(2, 8, 2) CASE(3, 16, 2) CASE(4, 32, 2) CASE(5, 32, 4) CASE(6, 32, 8)
+        SPFOM_BINS(CASE)
 #undef CASE
     }
 }
@@ -234,7 +256,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             maxc = cnt;
         }
         if (maxc == 0) continue;
-        primal_dispatch(b, argmax, S, L, maxc, h->sm_count, h->stream);
+        primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, h->sm_count, h->stream);
         ++nl;
     }
     CUDA_TRY(h, cudaGetLastError());
@@ -250,7 +272,7 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
     int full_mode = h->pl.sampled ? 0 : 1;
     if (refresh) {
         CUDA_TRY(h, cudaMemsetAsync(acc, 0, (h->N + 1) * 8, h->stream));
-        k_usage<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq, acc);
+        k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->nq, acc, (int32_t)std::min<int64_t>(kHeadMax, h->N));
         full_mode = 1;
         ++nl;
     }
@@ -400,7 +422,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     auto *h = new spfom_handle();
     h->pl = pl;
     h->params = *p;
-    if (h->params.max_newton <= 0) h->params.max_newton = 64;
+    if (h->params.max_newton <= 0) h->params.max_newton = 200;
     h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     if (h->stream == nullptr || h->stream == cudaStreamLegacy) {
         // the legacy default stream cannot be captured into a CUDA graph: use a private one
@@ -679,7 +701,7 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     DevState S = h->S;
     double *sf = slot_ptr<double>(h, O_TMP);
     CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));
-    k_usage<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq, sf);
+    k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->nq, sf, (int32_t)std::min<int64_t>(kHeadMax, h->N));
     spfom_status st = allreduce(h, sf, sf, (size_t)h->N, kNcclFloat64, kNcclSum);
     if (st != SPFOM_OK) return st;
     double *pseg = slot_ptr<double>(h, O_RESSEG);
@@ -740,6 +762,7 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     out->cert_upper = D;
     out->newton_failures = (int64_t)cnt[0];
     out->newton_passes = (int64_t)cnt[1];
+    out->newton_restarts = (int64_t)cnt[2];
     return SPFOM_OK;
 }
 

@@ -1,0 +1,124 @@
+// spfom_common.cuh -- device state, memory helpers and segment lists shared by
+// the SPFOM kernels (sm_100a, fp64).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+namespace spfom {
+
+constexpr int kThreads = 256;       // non-primal kernels
+constexpr int kPrimalThreads = 128; // K1: 4 warps per block, 4 blocks per SM
+#ifndef SPFOM_PRIMAL_MIN_BLOCKS
+#define SPFOM_PRIMAL_MIN_BLOCKS 3
+#endif
+constexpr int kPrimalMinBlocks = SPFOM_PRIMAL_MIN_BLOCKS;
+constexpr int kHeadMax = 1024;      // products privatised in shared memory (Zipf head)
+
+struct DevState {
+    // per quad (4 padded entries), relabelled product ids, rows sorted by new id
+    const int4 *pidx;     // [nq]
+    const double *v;      // [4 nq]  attraction (0 on pads)
+    const double *om;     // [4 nq]  omega = w / v (0 on pads)
+    double *y;            // [4 nq]  sales iterate
+    double *ybar;         // [4 nq]  average (averaging on) or null
+    // per local segment
+    const int32_t *qoff;  // [m+1] quad offsets
+    const double2 *seg;   // [m]   (lambda, vt0 = v0 + sum w)
+    double *y0;           // [m]   no-purchase iterate
+    double *y0bar;        // [m]   or null
+    double4 *warm;        // [m]   (nu, kappa, U, -) of the last projection
+    // per product, N + 1 slots (slot N = dummy of the pads: g = 0)
+    const double *r, *c, *tau;
+    double *eta, *g, *s, *s_prev, *etabar;
+    // counters (device)
+    unsigned long long *counters;  // [0] newton failures, [1] passes
+    int64_t *t;                    // completed iterations
+    int64_t m, N;
+    double theta, mu, omega_x;
+    int32_t max_newton;
+    int32_t sampled;               // 1 => scatter y_new - y_old into s (stale rows kept)
+};
+
+// ----------------------------------------------------------------- memory helpers
+__device__ __forceinline__ void ld256_nc(const double *p, double &a, double &b, double &c, double &d) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void ld256(const double *p, double &a, double &b, double &c, double &d) {
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void st256(double *p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+__device__ __forceinline__ int4 ld128_nc(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+// TMA bulk prefetch of a contiguous range into L2 (bytes: multiple of 16, 16-B aligned)
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
+__device__ __forceinline__ int idx_of(const int4 &q, int e) {
+    return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double x) {
+#pragma unroll
+    for (int o = G / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+template <int G>
+__device__ __forceinline__ double group_max(double x) {
+#pragma unroll
+    for (int o = G / 2; o >= 1; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+// ----------------------------------------------------------------- segment lists
+// Segments processed by a launch: ids[first .. first+count) (local ids) or,
+// ids == null, the contiguous range [first, first + count).  In sampled mode
+// the list is the (iteration row, bin) slice of the block table, found from *t.
+struct SegList {
+    const int32_t *ids;
+    int64_t first, count;
+    const int32_t *row_off;      // sampled: [block_iters][nbins+1] offsets into ids
+    int32_t bin, nbins;
+    int64_t block_iters;
+    int32_t head;                // K1: products [0, head) privatised in shared memory (0 = none)
+};
+
+__device__ __forceinline__ bool seg_slot(const SegList &L, const DevState &S, int64_t slot, int64_t &i) {
+    if (L.row_off) {
+        const int64_t row = (*S.t) % L.block_iters;
+        const int32_t *ro = L.row_off + row * (L.nbins + 1);
+        const int64_t a = ro[L.bin], b = ro[L.bin + 1];
+        if (slot >= b - a) return false;
+        i = L.ids[a + slot];
+        return true;
+    }
+    if (slot >= L.count) return false;
+    i = L.ids ? (int64_t)L.ids[L.first + slot] : L.first + slot;
+    return true;
+}
+
+__device__ __forceinline__ int64_t seg_count(const SegList &L, const DevState &S) {
+    if (L.row_off) {
+        const int64_t row = (*S.t) % L.block_iters;
+        const int32_t *ro = L.row_off + row * (L.nbins + 1);
+        return ro[L.bin + 1] - ro[L.bin];
+    }
+    return L.count;
+}
+
+}  // namespace spfom

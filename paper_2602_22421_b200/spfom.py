@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspfom.so")
+LIB_PATH = os.environ.get("SPFOM_LIB") or os.path.join(_HERE, "libspfom.so")
 
 STATUS = {0: "SPFOM_OK", 1: "SPFOM_EINVAL", 2: "SPFOM_EDATA", 3: "SPFOM_ENUMERIC", 4: "SPFOM_ECUDA",
           5: "SPFOM_ENCCL", 6: "SPFOM_ENOMEM"}
@@ -57,7 +57,7 @@ class _Residuals(C.Structure):
     _fields_ = [("iteration", C.c_int64)] + [(n, C.c_double) for n in (
         "primal_obj", "dual_obj", "rel_gap", "infeas_abs", "infeas_rel", "infeas_rel_l2", "balance_rel_max",
         "scale_rel_max", "neg_max", "compl_slack", "cert_lower", "cert_upper", "alpha")] + [
-        ("newton_failures", C.c_int64), ("newton_passes", C.c_int64)]
+        ("newton_failures", C.c_int64), ("newton_passes", C.c_int64), ("newton_restarts", C.c_int64)]
 
 
 class _Info(C.Structure):
@@ -125,7 +125,7 @@ class Params:
     averaging: bool = False
     blocks: Optional[np.ndarray] = None      # [iters][B] int32 global ids, rows sorted
     refresh_every: int = 0
-    max_newton: int = 64
+    max_newton: int = 200
 
     @staticmethod
     def converge(**kw) -> "Params":

@@ -238,3 +238,18 @@ def test_full_size_sampled_outputs(name):
     gpu.close()
     assert r["newton_failures"] == 0 and r["balance_rel_max"] <= 1e-12 and r["neg_max"] == 0.0
     del cpu
+
+
+def test_newton_budget_exhaustion_is_reported():
+    """Failure detection: with a 2-pass budget the projection cannot finish; the
+    next synchronising getter reports SPFOM_ENUMERIC and residuals count it."""
+    from paper_2602_22421_b200 import Solver, SpfomError
+    inst = generate("small", m=300, N=150, k=(5, 40))
+    gpu = Solver(inst, _params(max_newton=2))
+    gpu.step(3)
+    r = gpu.residuals()
+    assert r["newton_failures"] > 0
+    with pytest.raises(SpfomError) as ei:
+        gpu.duals()
+    assert ei.value.status == 3
+    gpu.close()
