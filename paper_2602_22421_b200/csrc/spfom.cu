@@ -152,7 +152,6 @@ struct spfom_handle {
     std::vector<int32_t> new2old, old2new;     // products
     std::vector<int64_t> pos_map;              // original entry -> padded entry
     std::vector<int32_t> bin_first;            // [kNumBins+1] offsets into bin ids
-    int bin_qmax[16] = {0};                    // longest row (quads) per bin: K1's TMA buffer size
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
     std::string err;
@@ -186,56 +185,36 @@ spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, in
 }
 
 // Persistent grid: at most (resident blocks per SM) x SMs blocks, each looping
-// over segments.  Shared memory = per-warp double TMA buffers (sized by the
-// bin's longest row, qmax quads) + the privatised Zipf head; the head size H
-// is the largest of 1024/512/256/128 that keeps kPrimalMinBlocks blocks
-// resident, and 0 when a block sees too few segments to amortise its flush.
+// over segments; the Zipf head is privatised only when a block sees enough
+// segments to amortise its flush (H REDs per block).
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
-void launch_primal(const DevState &S, SegList L, int64_t max_count, int qmax, int sm_count, cudaStream_t st) {
-    auto kern = k_primal<G, Q, ARGMAX, SAMPLED>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count, cudaStream_t st) {
+    static int resident = 0;
+    constexpr size_t smem = sizeof(PrimalSmem<Q>);
+    if (resident == 0) {
+        cudaFuncSetAttribute(k_primal<G, Q, ARGMAX, SAMPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_primal<G, Q, ARGMAX, SAMPLED>, kPrimalThreads, smem);
+        resident = std::max(resident, 1);
     }
     const int64_t groups_per_block = kPrimalThreads / G;
-    int H = 0, resident = 1;
-    size_t smem = 0;
-    const int heads[] = {kHeadMax, kHeadMax / 2, kHeadMax / 4, kHeadMax / 8, 0};
-    for (int hc : heads) {
-        const int Hc = (int)std::min<int64_t>(hc, S.N);
-        const PrimalLayout lay{Hc, qmax, G, 4 * Q};
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPrimalThreads, lay.total());
-        if (occ >= kPrimalMinBlocks || hc == 0) {
-            H = Hc;
-            smem = lay.total();
-            resident = std::max(occ, 1);
-            break;
-        }
-    }
     int64_t blocks = (max_count + groups_per_block - 1) / groups_per_block;
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count * resident));
     const int64_t segs_per_block = (max_count + blocks - 1) / blocks;
-    if (segs_per_block < 64 && H > 0) {
-        H = 0;
-        smem = PrimalLayout{0, qmax, G, 4 * Q}.total();
-    }
-    L.head = H;
-    kern<<<(unsigned)blocks, kPrimalThreads, smem, st>>>(S, L, qmax);
+    L.head = (segs_per_block >= 64) ? (int32_t)std::min<int64_t>(kHeadMax, S.N) : 0;
+    k_primal<G, Q, ARGMAX, SAMPLED><<<(unsigned)blocks, kPrimalThreads, smem, st>>>(S, L);
 }
 
-void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int qmax,
-                     int sms, cudaStream_t st) {
+void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int sms,
+                     cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q)                                                                      \
     case B:                                                                                \
         if (argmax) {                                                                      \
-            if (sampled) launch_primal<G, Q, true, true>(S, L, cnt, qmax, sms, st);        \
-            else launch_primal<G, Q, true, false>(S, L, cnt, qmax, sms, st);               \
+            if (sampled) launch_primal<G, Q, true, true>(S, L, cnt, sms, st);              \
+            else launch_primal<G, Q, true, false>(S, L, cnt, sms, st);                     \
         } else {                                                                           \
-            if (sampled) launch_primal<G, Q, false, true>(S, L, cnt, qmax, sms, st);       \
-            else launch_primal<G, Q, false, false>(S, L, cnt, qmax, sms, st);              \
+            if (sampled) launch_primal<G, Q, false, true>(S, L, cnt, sms, st);             \
+            else launch_primal<G, Q, false, false>(S, L, cnt, sms, st);                    \
         }                                                                                  \
         break;
         SPFOM_BINS(CASE)
@@ -277,7 +256,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             maxc = cnt;
         }
         if (maxc == 0) continue;
-        primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, h->bin_qmax[b], h->sm_count, h->stream);
+        primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, h->sm_count, h->stream);
         ++nl;
     }
     CUDA_TRY(h, cudaGetLastError());
@@ -539,8 +518,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
         seg[i] = make_double2(in->arrival[i], vt0);
         // initial projection multipliers (nu, kappa, U)
-        // .w mirrors y0 so that K1 fetches (nu, kappa, U, y0) as one 32-byte TMA copy
-        warm[i] = make_double4(0.0, 0.0, in->arrival[i] / (vt0 + svt), in->arrival[i]);
+        warm[i] = make_double4(0.0, 0.0, in->arrival[i] / (vt0 + svt), 0.0);
         if (!std::isfinite(vt0)) bad_numeric = true;
     }
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
@@ -551,12 +529,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     {
         std::vector<int64_t> cnt(kNumBins, 0);
         std::vector<int> segbin(m);
-        for (int64_t i = 0; i < m; ++i) {
-            const int nqi = qoff[i + 1] - qoff[i];
-            segbin[i] = bin_of(nqi);
-            cnt[segbin[i]]++;
-            h->bin_qmax[segbin[i]] = std::max(h->bin_qmax[segbin[i]], nqi);
-        }
+        for (int64_t i = 0; i < m; ++i) { segbin[i] = bin_of(qoff[i + 1] - qoff[i]); cnt[segbin[i]]++; }
         for (int b = 0; b < kNumBins; ++b) h->bin_first[b + 1] = (int32_t)(h->bin_first[b] + cnt[b]);
         std::vector<int64_t> fill(h->bin_first.begin(), h->bin_first.end() - 1);
         for (int64_t i = 0; i < m; ++i) binids[fill[segbin[i]]++] = (int32_t)i;
@@ -809,16 +782,7 @@ spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0,
         CUDA_TRY(h, cudaMemcpyAsync(h->S.y, tmp.data(), h->nq * 32, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
-    if (y0 && h->m) {
-        CUDA_TRY(h, cudaMemcpyAsync(h->S.y0, y0, h->m * 8, cudaMemcpyHostToDevice, h->stream));
-        // keep the y0 mirror in the warm-start records (.w) in step
-        std::vector<double4> w(h->m);
-        CUDA_TRY(h, cudaMemcpyAsync(w.data(), h->S.warm, h->m * 32, cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        for (int64_t i = 0; i < h->m; ++i) w[i].w = y0[i];
-        CUDA_TRY(h, cudaMemcpyAsync(h->S.warm, w.data(), h->m * 32, cudaMemcpyHostToDevice, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    }
+    if (y0) CUDA_TRY(h, cudaMemcpyAsync(h->S.y0, y0, h->m * 8, cudaMemcpyHostToDevice, h->stream));
     std::vector<double> t1(h->N + 1, 0.0), t2(h->N + 1, 0.0);
     if (eta) {
         std::vector<double> r(h->N + 1, 0.0);

@@ -10,37 +10,33 @@
 //      j < head goes to per-warp shared-memory histograms, flushed once per
 //      persistent block; the tail uses global fp64 reductions.
 //
-// Data movement: every warp runs its own two-stage TMA
-// pipeline.  A group of G lanes owns one segment per round; its leader issues
-// cp.async.bulk copies of the segment's padded quads (ids, v, omega, y), its
-// (lambda, vt0) record and its (nu, kappa, U, y0) record into the warp's
-// shared buffer for the round after next, completing on an mbarrier, so the
-// HBM stream never waits on the compute.  A quad = 4 entries; lane l of the
-// group holds quads l, l+G, .. (Q of them) in registers while it computes.
+// Thread mapping: a group of G lanes owns one segment; lane l holds quads
+// l, l+G, .. (Q of them) of the padded row; a quad = 4 entries = one 128-bit
+// id load + three 256-bit loads (v, omega, y).
 //
-// KKT system: with a_j = z_j - nu + omega_j kappa and the piece
-// C = {a_j >= v_j U} (capped), F = {0 < a_j < v_j U} (free):
+// KKT system: with a_j = z_j - nu + omega_j kappa and the
+// piece C = {a_j >= v_j U} (capped), F = {0 < a_j < v_j U} (free):
 //   R1 = sum_C v_j (a_j - v_j U) - vt0 kappa
 //   R2 = y0 + sum_j omega_j y_j - vt0 U,   R3 = y0 + sum_j y_j - lambda,
 //   y0 = z0 - nu + kappa, y_j = clamp(a_j, 0, v_j U).
-// The group sums are kept in piece-constant form: sum_C v a, sum_C v,
-// sum_C v omega, sum_C v^2, |F|, sum_F a, sum_F omega a, sum_F omega,
-// sum_F omega^2 (sum_j y = U sum_C v + sum_F a, sum_j omega y = U sum_C v omega
-// + sum_F omega a, R1 = sum_C v a - U sum_C v^2 - vt0 kappa).
+// Per piece everything is affine, so the group sums are kept in piece-constant
+// form: sum_C v a, sum_C v, sum_C v omega, sum_C v^2, |F|, sum_F a,
+// sum_F omega a, sum_F omega, sum_F omega^2 (then sum_j y = U sum_C v + sum_F a,
+// sum_j omega y = U sum_C v omega + sum_F omega a).
 //
 // Newton schedule per segment: a FULL pass evaluates the piece, R and the
 // Jacobian and takes the Newton step; the next pass is a CHECK pass that only
 // re-classifies: if no entry of the group changed class, R is affine on that
 // piece, so the new point solves R = 0 exactly and the segment is done without
 // any reduction.  Otherwise a FULL pass follows at the same point
-// (sufficient-decrease test, backtracking on ||R||_inf); after half the pass
-// budget a segment restarts from the cold point.
+// (sufficient-decrease test, backtracking on ||R||_inf).  Every pass also
+// produces y at its point, so the terminating pass yields the output.
 //
 // Head scatter: the warp's segments share one histogram, so their updates of
 // a hot product would collide.  Every lane stages its (id, contribution)
-// pairs in shared memory (in the just-consumed TMA buffer); then, one segment
-// at a time, all 32 lanes apply that segment's staged updates -- ids within a
-// segment are distinct, so a round has no conflicts and needs no atomics.
+// pairs in shared memory; then, one segment at a time, all 32 lanes apply
+// that segment's staged updates -- ids within a segment are distinct, so a
+// round has no conflicts and needs no atomics.
 #pragma once
 
 #include "spfom_common.cuh"
@@ -73,9 +69,10 @@ struct PieceSums {
 };
 
 // FULL pass, one entry: classify at (x0, x1, x2) = (nu, kappa, U), accumulate
-// the piece-constant sums, set the class bits (branch-free selects).
-__device__ __forceinline__ void full_entry(double z, double v, double om, double x0, double x1, double x2,
-                                           uint32_t bit, PieceSums &s, uint32_t &cm, uint32_t &fm) {
+// the piece-constant sums, set the class bits, return y_j (branch-free; ptxas
+// turns the selects into FSEL, which beats predicated fp64 here).
+__device__ __forceinline__ double full_entry(double z, double v, double om, double x0, double x1, double x2,
+                                             uint32_t bit, PieceSums &s, uint32_t &cm, uint32_t &fm) {
     const double a = fma(om, x1, z - x0);     // a = omega kappa + (z - nu)
     const double cap = v * x2;                // v U
     const bool isC = a >= cap;
@@ -85,18 +82,19 @@ __device__ __forceinline__ void full_entry(double z, double v, double om, double
     const double vc = isC ? v : 0.0;
     const double af = isF ? a : 0.0;
     const double wf = isF ? om : 0.0;
-    s.rva = fma(vc, a, s.rva);
-    s.cv += vc;
-    s.cvw = fma(vc, om, s.cvw);
-    s.cvv = fma(vc, v, s.cvv);
-    s.sfa += af;
-    s.sfwa = fma(om, af, s.sfwa);
-    s.fw += wf;
-    s.fww = fma(wf, om, s.fww);
+    s.rva = fma(vc, a, s.rva);                // sum_C v a
+    s.cv += vc;                               // sum_C v
+    s.cvw = fma(vc, om, s.cvw);               // sum_C v omega
+    s.cvv = fma(vc, v, s.cvv);                // sum_C v^2
+    s.sfa += af;                              // sum_F a
+    s.sfwa = fma(om, af, s.sfwa);             // sum_F omega a
+    s.fw += wf;                               // sum_F omega
+    s.fww = fma(wf, om, s.fww);               // sum_F omega^2
     s.nf += isF ? 1 : 0;
+    return isC ? cap : af;
 }
 
-// CHECK pass / output, one entry: class bits and y_j at (x0, x1, x2).
+// CHECK pass, one entry: class bits and y_j at (x0, x1, x2) only.
 __device__ __forceinline__ double check_entry(double z, double v, double om, double x0, double x1, double x2,
                                               uint32_t bit, uint32_t &cm, uint32_t &fm) {
     const double a = fma(om, x1, z - x0);
@@ -108,183 +106,82 @@ __device__ __forceinline__ double check_entry(double z, double v, double om, dou
     return isC ? cap : (isF ? a : 0.0);
 }
 
-__device__ __forceinline__ void lds256(const double *p, double &a, double &b, double &c, double &d) {
-    const double2 u = reinterpret_cast<const double2 *>(p)[0];
-    const double2 w = reinterpret_cast<const double2 *>(p)[1];
-    a = u.x; b = u.y; c = w.x; d = w.y;
-}
-
-// Shared-memory layout of K1 (byte sizes; host and device agree through these).
-// A warp buffer holds the round's GPW segments packed: [seg 16 x GPW][warm 32 x
-// GPW][ids 16 x QW][v 32 x QW][omega 32 x QW][y 32 x QW], QW = GPW * qmax
-// quads, each segment's quads at its packed offset; consecutive segments
-// arrive as one copy per array.
-struct PrimalLayout {
-    int H, qmax, G, NE;
-    __host__ __device__ int warps() const { return kPrimalThreads / 32; }
-    __host__ __device__ int gpw() const { return 32 / G; }
-    __host__ __device__ uint32_t qw() const { return (uint32_t)gpw() * (uint32_t)qmax; }
-    __host__ __device__ uint32_t off_warm() const { return 16u * gpw(); }
-    __host__ __device__ uint32_t off_ids() const { return 48u * gpw(); }
-    __host__ __device__ uint32_t off_v() const { return off_ids() + 16u * qw(); }
-    __host__ __device__ uint32_t off_om() const { return off_v() + 32u * qw(); }
-    __host__ __device__ uint32_t off_y() const { return off_om() + 32u * qw(); }
-    __host__ __device__ uint32_t stage_bytes() const { return 32u * (uint32_t)NE * 12u; }
-    __host__ __device__ uint32_t buf_bytes() const {
-        const uint32_t a = off_y() + 32u * qw(), b = stage_bytes();
-        return ((a > b ? a : b) + 127u) & ~127u;
-    }
-    __host__ __device__ size_t off_ghead() const { return (size_t)warps() * H * 8; }
-    __host__ __device__ size_t off_mbar() const { return ((off_ghead() + (size_t)H * 8 + 15) / 16) * 16; }
-    __host__ __device__ size_t off_meta() const { return off_mbar() + (size_t)warps() * 2 * 8; }
-    __host__ __device__ size_t off_bufs() const {
-        return ((off_meta() + (size_t)warps() * 2 * gpw() * 16 + 127) / 128) * 128;
-    }
-    __host__ __device__ size_t total() const { return off_bufs() + (size_t)warps() * 2 * buf_bytes(); }
+template <int Q>
+struct PrimalSmem {
+    static constexpr int WARPS = kPrimalThreads / 32;
+    static constexpr int NE = 4 * Q;
+    double hist[WARPS][kHeadMax];          // per-warp usage of the head products
+    double ghead[kHeadMax];                // price vector g on the head products
+    double stage_val[WARPS][32 * NE];      // staged head contributions, [warp][e * 32 + lane]
+    int stage_idx[WARPS][32 * NE];
 };
 
+// Resident blocks per SM the register budget targets: one quad per lane fits 4
+// blocks (128 registers), wider lanes 3.
+template <int Q>
+constexpr int primal_min_blocks() { return kPrimalMinBlocks; }
+
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
-__global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(DevState S, SegList L, int qmax) {
+__global__ void __launch_bounds__(kPrimalThreads, primal_min_blocks<Q>()) k_primal(DevState S, SegList L) {
     constexpr int NE = 4 * Q;               // entries per lane
     constexpr int GPW = 32 / G;             // segments per warp
     constexpr int WARPS = kPrimalThreads / 32;
     static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
 
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int H = L.head;
-    const PrimalLayout lay{H, qmax, G, NE};
-    double *hist_all = reinterpret_cast<double *>(smem);
-    double *ghead = reinterpret_cast<double *>(smem + lay.off_ghead());
-    uint64_t *mbar_all = reinterpret_cast<uint64_t *>(smem + lay.off_mbar());
-    int4 *meta_all = reinterpret_cast<int4 *>(smem + lay.off_meta());
-    unsigned char *bufs_all = smem + lay.off_bufs();
-    const uint32_t buf_bytes = lay.buf_bytes();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PrimalSmem<Q> &sm = *reinterpret_cast<PrimalSmem<Q> *>(smem_raw);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const int gidx = lane / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gidx * G));
+    const int H = L.head;
 
     for (int j = threadIdx.x; j < H; j += kPrimalThreads) {
-        ghead[j] = S.g[j];
+        sm.ghead[j] = S.g[j];
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) hist_all[w * H + j] = 0.0;
-    }
-    uint64_t *mbar = mbar_all + warp * 2;
-    if (lane == 0) {
-        mbar_init(mbar + 0, 1);
-        mbar_init(mbar + 1, 1);
-        fence_mbar_init();
+        for (int w = 0; w < WARPS; ++w) sm.hist[w][j] = 0.0;
     }
     __syncthreads();
-    double *hw = hist_all + warp * H;
-    int4 *meta = meta_all + warp * 2 * GPW;
-    unsigned char *bufs = bufs_all + (size_t)warp * 2 * buf_bytes;
+    double *hw = sm.hist[warp];
+    double *stv = sm.stage_val[warp];
+    int *sti = sm.stage_idx[warp];
 
     const int64_t groups_per_block = kPrimalThreads / G;
     const int64_t total = seg_count(L, S);
     const int64_t stride = (int64_t)gridDim.x * groups_per_block;
-    const int64_t rounds = (total + stride - 1) / stride;                // warp-uniform
-    const int64_t wslot0 = (int64_t)blockIdx.x * groups_per_block + warp * GPW;   // the warp's first slot
+    const int64_t slot_end = ((total + stride - 1) / stride) * stride;   // warp-uniform trip count
     unsigned long long passes_acc = 0, fail_acc = 0, restart_acc = 0;
 
-    // producer (lane 0): fetch round r's GPW segments into buffer r & 1.
-    // meta[b][gg] = (segment id, first quad, quad count, packed quad offset or -1)
-    auto issue = [&](int64_t r) {
-        if (lane != 0) return;
-        const int b = (int)(r & 1);
-        unsigned char *buf = bufs + (size_t)b * buf_bytes;
-        int64_t ids[GPW];
-        int32_t qa[GPW], qb[GPW];
-        bool consecutive = true;
-        uint32_t tx = 0, lq = 0;
-#pragma unroll
-        for (int gg = 0; gg < GPW; ++gg) {
-            int64_t i = 0;
-            const bool act = seg_slot(L, S, wslot0 + gg + r * stride, i);
-            ids[gg] = act ? i : -1;
-            qa[gg] = act ? S.qoff[i] : 0;
-            qb[gg] = act ? S.qoff[i + 1] : 0;
-            const uint32_t nq = (uint32_t)(qb[gg] - qa[gg]);
-            meta[b * GPW + gg] = make_int4((int)i, qa[gg], (int)nq, act ? (int)lq : -1);
-            if (act) tx += 48u + 112u * nq;
-            lq += nq;
-            consecutive = consecutive && act && (gg == 0 || ids[gg] == ids[gg - 1] + 1);
-        }
-        mbar_arrive_expect_tx(mbar + b, tx);
-        if (consecutive) {
-            // one copy per array for the warp's consecutive segments
-            const int64_t i0 = ids[0];
-            const int32_t q0 = qa[0];
-            bulk_g2s(buf, S.seg + i0, 16u * GPW, mbar + b);
-            bulk_g2s(buf + lay.off_warm(), S.warm + i0, 32u * GPW, mbar + b);
-            if (lq) {
-                bulk_g2s(buf + lay.off_ids(), S.pidx + q0, 16u * lq, mbar + b);
-                bulk_g2s(buf + lay.off_v(), S.v + 4 * (int64_t)q0, 32u * lq, mbar + b);
-                bulk_g2s(buf + lay.off_om(), S.om + 4 * (int64_t)q0, 32u * lq, mbar + b);
-                bulk_g2s(buf + lay.off_y(), S.y + 4 * (int64_t)q0, 32u * lq, mbar + b);
-            }
-        } else {
-            uint32_t off = 0;
-#pragma unroll
-            for (int gg = 0; gg < GPW; ++gg) {
-                if (ids[gg] < 0) continue;
-                const int64_t i = ids[gg];
-                const int32_t q0 = qa[gg];
-                const uint32_t nq = (uint32_t)(qb[gg] - q0);
-                bulk_g2s(buf + 16u * gg, S.seg + i, 16u, mbar + b);
-                bulk_g2s(buf + lay.off_warm() + 32u * gg, S.warm + i, 32u, mbar + b);
-                if (nq) {
-                    bulk_g2s(buf + lay.off_ids() + 16u * off, S.pidx + q0, 16u * nq, mbar + b);
-                    bulk_g2s(buf + lay.off_v() + 32u * off, S.v + 4 * (int64_t)q0, 32u * nq, mbar + b);
-                    bulk_g2s(buf + lay.off_om() + 32u * off, S.om + 4 * (int64_t)q0, 32u * nq, mbar + b);
-                    bulk_g2s(buf + lay.off_y() + 32u * off, S.y + 4 * (int64_t)q0, 32u * nq, mbar + b);
-                }
-                off += nq;
-            }
-        }
-    };
-    if (rounds > 0) issue(0);
-    if (rounds > 1) issue(1);
+    for (int64_t slot = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; slot < slot_end; slot += stride) {
+        int64_t i = 0;
+        const bool active = seg_slot(L, S, slot, i);
 
-    for (int64_t r = 0; r < rounds; ++r) {
-        const int b = (int)(r & 1);
-        mbar_wait(mbar + b, (uint32_t)((r >> 1) & 1));
-        const int4 mt = meta[b * GPW + gidx];
-        const int64_t i = mt.x;
-        const bool active = mt.w >= 0;
-        const int32_t q0 = mt.y, nq = mt.z, lq = mt.w;
-        const unsigned char *buf = bufs + (size_t)b * buf_bytes;
-
-        // ---- segment scalars and this lane's quads (from shared memory)
+        // ---- segment scalars and this lane's quads
         double lam = 1.0, vt0 = 1.0, z0 = 1.0;
-        double4 wm = make_double4(0.0, 0.0, 1.0, 1.0);
+        int32_t q0 = 0, q1 = 0;
         if (active) {
-            const double2 sv = reinterpret_cast<const double2 *>(buf)[gidx];
+            const double2 sv = S.seg[i];
             lam = sv.x;
             vt0 = sv.y;
-            const double2 *wp = reinterpret_cast<const double2 *>(buf + lay.off_warm()) + 2 * gidx;
-            const double2 w01 = wp[0], w23 = wp[1];
-            wm = make_double4(w01.x, w01.y, w23.x, w23.y);
-            z0 = wm.w;
+            z0 = S.y0[i];
+            q0 = S.qoff[i];
+            q1 = S.qoff[i + 1];
         }
         int idx[NE];
         double v[NE], om[NE], z[NE];
         double yold[SAMPLED ? NE : 1];
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const int32_t q = gl + G * t;
+            const int32_t q = q0 + gl + G * t;
             double y4[4] = {0.0, 0.0, 0.0, 0.0};
-            if (active && q < nq) {
-                const int32_t p = lq + q;
-                const int4 id4 = reinterpret_cast<const int4 *>(buf + lay.off_ids())[p];
+            if (q < q1) {
+                const int4 id4 = ld128_nc(S.pidx + q);
                 idx[4 * t + 0] = id4.x; idx[4 * t + 1] = id4.y; idx[4 * t + 2] = id4.z; idx[4 * t + 3] = id4.w;
-                lds256(reinterpret_cast<const double *>(buf + lay.off_v()) + 4 * p, v[4 * t], v[4 * t + 1],
-                       v[4 * t + 2], v[4 * t + 3]);
-                lds256(reinterpret_cast<const double *>(buf + lay.off_om()) + 4 * p, om[4 * t], om[4 * t + 1],
-                       om[4 * t + 2], om[4 * t + 3]);
-                lds256(reinterpret_cast<const double *>(buf + lay.off_y()) + 4 * p, y4[0], y4[1], y4[2], y4[3]);
+                ld256_nc(S.v + 4 * (int64_t)q, v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+                ld256_nc(S.om + 4 * (int64_t)q, om[4 * t], om[4 * t + 1], om[4 * t + 2], om[4 * t + 3]);
+                ld256(S.y + 4 * (int64_t)q, y4[0], y4[1], y4[2], y4[3]);
             } else {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -303,14 +200,13 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
-            const double gj = (j < H) ? ghead[j] : __ldg(S.g + j);
+            const double gj = (j < H) ? sm.ghead[j] : __ldg(S.g + j);
             if constexpr (ARGMAX) z[e] = gj;             // theta = inf: keep g itself
             else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
         }
 
-        double yv[NE];                          // y at the final point
+        double yv[NE];                          // y at the terminating point
         double y0new;
-        double x0 = 0.0, x1 = 0.0, x2 = 1.0;
         if constexpr (ARGMAX) {
             // ---- exact inner argmax, Dinkelbach from z = 0 (reading c6)
             double zs = 0.0, den = 0.0, sv_in = 0.0;
@@ -347,7 +243,8 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
             sabs = group_sum<G>(sabs);
             const double tol = 1e-13 * (lam + fabs(z0) + sabs) * fmax(1.0, vt0);
 
-            x0 = wm.x; x1 = wm.y; x2 = wm.z;                    // trial point (nu, kappa, U)
+            const double4 wm = active ? S.warm[i] : make_double4(0.0, 0.0, 1.0, 0.0);
+            double x0 = wm.x, x1 = wm.y, x2 = wm.z;             // trial point (nu, kappa, U)
             double a0 = x0, a1 = x1, a2 = x2;                   // last accepted point
             double d0 = 0.0, d1 = 0.0, d2 = 0.0, step = 1.0, Ra = 0.0;
             uint32_t cA = 0, fA = 0;                            // class bitmasks at the accepted point
@@ -383,7 +280,7 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
                 PieceSums ps = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
                 if (need) {
 #pragma unroll
-                    for (int e = 0; e < NE; ++e) full_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, ps, cm, fm);
+                    for (int e = 0; e < NE; ++e) (void)full_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, ps, cm, fm);
                     ps.sfa = group_sum<G>(ps.sfa);   ps.sfwa = group_sum<G>(ps.sfwa);
                     ps.rva = group_sum<G>(ps.rva);   ps.cv = group_sum<G>(ps.cv);
                     ps.cvw = group_sum<G>(ps.cvw);   ps.cvv = group_sum<G>(ps.cvv);
@@ -435,7 +332,8 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
                                 if (step < 1e-12) { done = true; failed = true; }
                             }
                             if (!done && passes >= S.max_newton) {
-                                done = true;                  // budget spent: keep the last evaluated point
+                                // budget spent: keep the last evaluated point
+                                done = true;
                                 failed = true;
                             }
                             if (!done) {
@@ -453,6 +351,7 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
                 passes_acc += (unsigned long long)passes;
                 fail_acc += failed ? 1ull : 0ull;
                 restart_acc += restarted ? 1ull : 0ull;
+                S.warm[i] = make_double4(x0, x1, x2, 0.0);
             }
             uint32_t cm = 0, fm = 0;
 #pragma unroll
@@ -460,15 +359,12 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
             y0new = z0 - x0 + x1;
         }
 
-        // ---- write back, a5 usage scatter (tail: global RED; head: staged in this round's buffer)
-        __syncwarp();                                   // every lane is done reading buffer b
-        double *stv = reinterpret_cast<double *>(bufs + (size_t)b * buf_bytes);
-        int *sti = reinterpret_cast<int *>(stv + 32 * NE);
+        // ---- write back, a5 usage scatter (tail: global RED; head: staged)
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
-            const int32_t q = gl + G * t;
-            const bool ok = active && q < nq;
-            if (ok) st256(S.y + 4 * (int64_t)(q0 + q), yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
+            const int32_t q = q0 + gl + G * t;
+            const bool ok = active && q < q1;
+            if (ok) st256(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int k = 4 * t + e;
@@ -480,12 +376,9 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
                 sti[k * 32 + lane] = j < H ? j : -1;
             }
         }
-        if (active && gl == 0) {
-            S.y0[i] = y0new;
-            S.warm[i] = make_double4(x0, x1, x2, y0new);
-        }
-        __syncwarp();
+        if (active && gl == 0) S.y0[i] = y0new;
         if (H > 0) {
+            __syncwarp();
             // one segment of the warp at a time; its G*NE staged updates hit distinct ids
 #pragma unroll
             for (int gg = 0; gg < GPW; ++gg) {
@@ -497,12 +390,6 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
                 }
                 __syncwarp();
             }
-        }
-        // refill this buffer with the round after next
-        if (r + 2 < rounds) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            issue(r + 2);
         }
     }
     if constexpr (!ARGMAX) {
@@ -516,7 +403,7 @@ __global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(Dev
     for (int j = threadIdx.x; j < H; j += kPrimalThreads) {
         double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) sum += hist_all[w * H + j];
+        for (int w = 0; w < WARPS; ++w) sum += sm.hist[w][j];
         if (sum != 0.0) atomicAdd(S.s + j, sum);
     }
 }
