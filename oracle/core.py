@@ -72,6 +72,10 @@ def lib():
         L.oracle_iterate.restype = C.c_int
         L.oracle_iterate.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), _dp, C.c_void_p, C.c_int64,
                                      C.POINTER(_State)]
+        L.oracle_primal_shard.restype = C.c_int
+        L.oracle_primal_shard.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), C.POINTER(_State), _dp]
+        L.oracle_dual_apply.restype = None
+        L.oracle_dual_apply.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), _dp, _dp, C.POINTER(_State)]
         L.oracle_residuals.restype = C.c_int
         L.oracle_residuals.argtypes = [C.POINTER(_Inst), _dp, _dp, _dp, C.c_void_p, _dp]
         _lib = L
@@ -193,6 +197,20 @@ class OracleSolver:
                                       blk.ctypes.data, blk.shape[0], C.byref(self._state))
         if rc != 0:
             raise FloatingPointError(f"oracle_iterate failed at t={self.t} (status {rc})")
+
+    # --- sharded emulation (Alg. 3): the caller sums the ranks' usage ---------
+    def primal_shard(self) -> np.ndarray:
+        """Full-sweep primal step of this (shard) instance; returns its usage."""
+        s_local = np.zeros(self.inst.N)
+        rc = lib().oracle_primal_shard(C.byref(self._inst), C.byref(self._params), C.byref(self._state), s_local)
+        if rc != 0:
+            raise FloatingPointError(f"oracle_primal_shard failed (status {rc})")
+        return s_local
+
+    def dual_apply(self, s_global: np.ndarray) -> None:
+        """Dual step with the global usage (identical on every rank)."""
+        lib().oracle_dual_apply(C.byref(self._inst), C.byref(self._params), self.tau_j, _f64(s_global),
+                                C.byref(self._state))
 
     def run(self, iters: int, blocks: Optional[np.ndarray] = None) -> None:
         for t in range(iters):

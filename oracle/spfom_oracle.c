@@ -475,6 +475,38 @@ int oracle_iterate(const oracle_instance *in, const oracle_params *p, const doub
     return rc;
 }
 
+/* Sharded emulation (Alg. 3): a rank owns a
+ * contiguous segment range (`in` is that shard).  oracle_primal_shard runs the
+ * full-sweep primal step of its segments and writes the shard's usage
+ * s_local = sum_{i in shard} y_i (i order); the caller sums the ranks' s_local
+ * and oracle_dual_apply performs the dual step every rank performs identically
+ * with that global usage.  Composed on one rank they are oracle_iterate's full
+ * sweep without averaging. */
+int oracle_primal_shard(const oracle_instance *in, const oracle_params *p, oracle_state *st, double *s_local) {
+    int64_t m = in->m, N = in->N, kmax = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t k = in->seg_ptr[i + 1] - in->seg_ptr[i];
+        if (k > kmax) kmax = k;
+    }
+    double *g = (double *)malloc((size_t)N * sizeof(double));
+    double *zb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
+    double *gb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
+    double *yb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
+    int rc = OR_OK;
+    for (int64_t j = 0; j < N; ++j) g[j] = in->r[j] - st->eta[j];
+    for (int64_t i = 0; i < m && rc == OR_OK; ++i) rc = update_segment(in, p, g, i, st, zb, gb, yb);
+    fresh_usage(in, st->y, s_local);
+    free(g); free(zb); free(gb); free(yb);
+    return rc;
+}
+
+void oracle_dual_apply(const oracle_instance *in, const oracle_params *p, const double *tau_j,
+                       const double *s_new, oracle_state *st) {
+    oracle_dual_step(in->N, st->eta, s_new, st->s, in->c, tau_j, p->mu, p->extrapolation);
+    for (int64_t j = 0; j < in->N; ++j) st->s[j] = s_new[j];
+    st->t += 1;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Residuals and certificate (reading c11).  out[0..12]:
  *  0 primal_obj P = sum_j r_j s_j (s = fresh A y)

@@ -340,6 +340,31 @@ def test_averaging_is_uniform_mean_of_iterates():
     assert np.abs(A.etabar - np.mean(etas, axis=0)).max() <= 1e-13 * max(1, np.abs(A.etabar).max())
 
 
+def test_shard_primitives_compose_to_iterate():
+    """primal_shard + dual_apply on the whole instance is oracle_iterate's full
+    sweep (the primitives used by the sharded emulation), bit for bit."""
+    inst = generate("small", m=200, N=120, k=(5, 40))
+    A = oracle.OracleSolver(inst)
+    B = oracle.OracleSolver(inst)
+    for _ in range(15):
+        A.step()
+        B.dual_apply(B.primal_shard())
+        assert np.array_equal(A.y, B.y) and np.array_equal(A.eta, B.eta) and np.array_equal(A.s, B.s)
+
+
+def test_oracle_reaches_small_lp_optimum():
+    """Converge preset on the BASELINE small config (seed 2), 3000 iterations, vs
+    the HiGHS optimum stored by tests/golden/make_lp_optima.py (oracle-only script)."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lp_optima.json")))["small"]
+    inst = generate("small")
+    S = oracle.OracleSolver(inst)
+    S.run(3000)
+    res = S.residuals()
+    assert abs(res["primal_obj"] - gold["Pstar"]) <= 1e-6 * gold["Pstar"]
+    assert res["infeas_rel"] <= 1e-6
+    assert res["cert_lower"] <= gold["Pstar"] * (1 + 1e-9) <= res["cert_upper"] * (1 + 2e-9)
+
+
 def test_multi_period_T1_and_stacking():
     """c15: T = 1 multi-period == single period; stacked P* == sum over the
     period LP with shared capacities solved directly (dense simplex on the
