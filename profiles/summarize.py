@@ -1,0 +1,94 @@
+"""Summarise ncu outputs into profiles/ (run here, no GPU needed).
+
+  python profiles/summarize.py ROUND gpurun_out/prof_k1.ncu-rep gpurun_out/launches.csv
+
+writes profiles/<ROUND>_k1_full.txt (key metrics, stall reasons, instruction
+mix), profiles/<ROUND>_launches.csv (the per-launch list) and updates
+profiles/ncu_summary.json (DRAM bytes per K1 launch, read by bench.py's
+roofline.traffic).
+"""
+import collections
+import csv
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_srcunit_tex_op_red.sum",
+        "smsp__inst_executed_op_global_red.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active"]
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def raw_metrics(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[h.index("Kernel Name")]}
+        for k in KEYS:
+            if k in h:
+                d[k] = (r[h.index(k)], units[h.index(k)])
+        res.append(d)
+    return res
+
+
+def sass_profile(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, data = rows[1], rows[2:]
+    iI, iS, iSrc = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
+    stall_cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    tot_s = sum(float(r[iS] or 0) for r in data) or 1.0
+    stalls = {c: sum(float(r[h.index(c)] or 0) for r in data) / tot_s * 100 for c in stall_cols}
+    tot_i = sum(float(r[iI] or 0) for r in data) or 1.0
+    ops = collections.Counter()
+    for r in data:
+        s = re.sub(r"^@!?U?P\w+\s+", "", r[iSrc].strip())
+        ops[s.split(" ")[0] if s else "?"] += float(r[iI] or 0)
+    mix = {k: v / tot_i * 100 for k, v in ops.most_common(20)}
+    sass_tags = sorted({op for op in ops if re.match(r"(UTC|UBLK|UTMA|LDTM|STTM|HMMA|REDG|RED|ATOM)", op)})
+    return stalls, mix, sass_tags
+
+
+def main():
+    rnd, rep = sys.argv[1], sys.argv[2]
+    launches = sys.argv[3] if len(sys.argv) > 3 else None
+    mets = raw_metrics(rep)
+    stalls, mix, tags = sass_profile(rep)
+    lines = [f"ncu --set full capture of K1 ({os.path.basename(rep)}), round {rnd}", ""]
+    for m in mets:
+        lines.append(f"kernel: {m['kernel']}")
+        for k in KEYS:
+            if k in m:
+                lines.append(f"  {k:62s} {m[k][0]} {m[k][1]}")
+    lines.append("")
+    lines.append("stall reasons (% of samples): " + ", ".join(f"{k} {v:.1f}" for k, v in
+                                                            sorted(stalls.items(), key=lambda x: -x[1])[:10]))
+    lines.append("instruction mix (% of executed): " + ", ".join(f"{k} {v:.1f}" for k, v in mix.items()))
+    lines.append("notable SASS ops present: " + ", ".join(tags))
+    open(os.path.join(HERE, f"{rnd}_k1_full.txt"), "w").write("\n".join(lines) + "\n")
+    m = mets[0]
+    rd = float(m["dram__bytes_read.sum"][0]) * UNIT[m["dram__bytes_read.sum"][1]]
+    wr = float(m["dram__bytes_write.sum"][0]) * UNIT[m["dram__bytes_write.sum"][1]]
+    summ_path = os.path.join(HERE, "ncu_summary.json")
+    summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+    summ["k_primal"] = {"round": rnd, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                        "duration": m["gpu__time_duration.sum"], "source": os.path.basename(rep)}
+    json.dump(summ, open(summ_path, "w"), indent=1)
+    if launches:
+        shutil.copy(launches, os.path.join(HERE, f"{rnd}_launches.csv"))
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
