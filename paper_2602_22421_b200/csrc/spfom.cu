@@ -91,10 +91,17 @@ struct Plan {
 };
 
 enum Slot {
-    O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEG, O_Y0, O_Y0BAR, O_WARM, O_R, O_C, O_TAU, O_ETA, O_G,
-    O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BINIDS, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
+    O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
+    O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
     O_COUNTS, O_NSLOTS
 };
+
+constexpr int kSpreadCopies = SPFOM_SPREAD_C;
+#ifndef SPFOM_SPREAD_N
+#define SPFOM_SPREAD_N 16384
+#endif
+int64_t spread_range(int64_t N) { return kSpreadCopies > 0 ? std::min<int64_t>(N, SPFOM_SPREAD_N) : 0; }
+int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spread slot after the N + 1 acc slots
 
 void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     pl.m = in->num_segments;
@@ -115,14 +122,14 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_PIDX] = nq * 16;
     sz[O_V] = sz[O_OM] = sz[O_Y] = nq * 32;
     sz[O_YBAR] = pl.averaging ? nq * 32 : 0;
-    sz[O_QOFF] = (m + 1) * 4;
-    sz[O_SEG] = m * 16;
-    sz[O_Y0] = m * 8;
+    sz[O_QOFF] = (m + 1 + 64) * 4;           // + slack: K1's 16-B qoff windows may read past the end
+    sz[O_SEGC] = m * 16;
+    sz[O_SEGV] = m * 32;
     sz[O_Y0BAR] = pl.averaging ? m * 8 : 0;
-    sz[O_WARM] = m * 32;
-    sz[O_R] = sz[O_C] = sz[O_TAU] = sz[O_ETA] = sz[O_G] = sz[O_ACC] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
+    sz[O_R] = sz[O_C] = sz[O_TAU] = sz[O_ETA] = sz[O_G] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
+    sz[O_ACC] = (spread_off(pl.N) + (size_t)kSpreadCopies * spread_range(pl.N)) * 8;   // acc, then spread copies
     sz[O_ETABAR] = pl.averaging ? N1 * 8 : 0;
-    sz[O_BINIDS] = m * 4;
+
     sz[O_BLKIDS] = std::max<int64_t>(pl.block_entries, 1) * 4;
     sz[O_ROWOFF] = pl.sampled ? p->block_iters * (kNumBins + 1) * 4 : 4;
     sz[O_RESSEG] = (size_t)kNumBins * kResidBlocks * 4 * 8;
@@ -151,7 +158,8 @@ struct spfom_handle {
     int64_t nq = 0, m = 0, N = 0, nnz = 0, n_present = 0;
     std::vector<int32_t> new2old, old2new;     // products
     std::vector<int64_t> pos_map;              // original entry -> padded entry
-    std::vector<int32_t> bin_first;            // [kNumBins+1] offsets into bin ids
+    std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
+    std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
     std::string err;
@@ -190,7 +198,7 @@ spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, in
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
 void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count, cudaStream_t st) {
     static int resident = 0;
-    constexpr size_t smem = sizeof(PrimalSmem<Q>);
+    constexpr size_t smem = sizeof(ListSmem<Q, G>);
     if (resident == 0) {
         cudaFuncSetAttribute(k_primal<G, Q, ARGMAX, SAMPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_primal<G, Q, ARGMAX, SAMPLED>, kPrimalThreads, smem);
@@ -202,6 +210,41 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
     const int64_t segs_per_block = (max_count + blocks - 1) / blocks;
     L.head = (segs_per_block >= 64) ? (int32_t)std::min<int64_t>(kHeadMax, S.N) : 0;
     k_primal<G, Q, ARGMAX, SAMPLED><<<(unsigned)blocks, kPrimalThreads, smem, st>>>(S, L);
+}
+
+// Full sweep of a contiguous bin: one persistent 12-warp block per SM; the
+// rest of the opt-in shared memory stages the head of g.
+template <int G, int Q, bool ARGMAX>
+void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
+    static int hg_cap = -1;
+    constexpr size_t fixed = stream_smem_fixed<G, Q>();
+    if (hg_cap < 0) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
+        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(fixed + (size_t)hg_cap * 8));
+    }
+    L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
+    L.hh = (int32_t)std::min<int64_t>(StreamLayout<G, Q>::HH, S.N);
+    const int64_t rounds = (L.count + StreamLayout<G, Q>::GPW - 1) / StreamLayout<G, Q>::GPW;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + kStreamWarps - 1) / kStreamWarps));
+    k_primal_stream<G, Q, ARGMAX><<<(unsigned)blocks, kStreamThreads, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+}
+
+void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
+    switch (b) {
+#define CASE(B, G, Q)                                                                      \
+    case B:                                                                                \
+        if constexpr (Q <= 2) {                                                            \
+            if (argmax) launch_stream<G, Q, true>(S, L, sms, st);                          \
+            else launch_stream<G, Q, false>(S, L, sms, st);                                \
+        }                                                                                  \
+        break;
+        SPFOM_BINS(CASE)
+#undef CASE
+    }
 }
 
 void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int sms,
@@ -248,10 +291,19 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             L.block_iters = h->params.block_iters;
             maxc = h->pl.bin_count[b] > 0 ? std::min<int64_t>(h->pl.bin_count[b], h->params.block_size) : 0;
         } else {
+            // full sweep: the bin is the contiguous device range [bin_first[b], bin_first[b+1])
             const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];
-            bool contiguous = (cnt == h->m);                    // one bin holds every segment: identity list
-            L.ids = contiguous ? nullptr : slot_ptr<int32_t>(h, O_BINIDS);
-            L.first = contiguous ? 0 : h->bin_first[b];
+            if (cnt == 0) continue;
+            if (kBins[b].Q <= 2) {
+                StreamList SL{};
+                SL.first = h->bin_first[b];
+                SL.count = cnt;
+                stream_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
+                ++nl;
+                continue;
+            }
+            L.ids = nullptr;
+            L.first = h->bin_first[b];
             L.count = cnt;
             maxc = cnt;
         }
@@ -272,8 +324,15 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
     int full_mode = h->pl.sampled ? 0 : 1;
     if (refresh) {
         CUDA_TRY(h, cudaMemsetAsync(acc, 0, (h->N + 1) * 8, h->stream));
+        if (S.spread_n > 0)
+            CUDA_TRY(h, cudaMemsetAsync(S.spread, 0, (size_t)S.spread_c * S.spread_n * 8, h->stream));
         k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->nq, acc, (int32_t)std::min<int64_t>(kHeadMax, h->N));
         full_mode = 1;
+        ++nl;
+    }
+    if (h->world > 1 && S.spread_n > 0) {
+        // fold the spread copies into acc before the cross-rank sum
+        k_fold<<<std::max<int64_t>(1, (S.spread_n + kThreads - 1) / kThreads), kThreads, 0, h->stream>>>(S);
         ++nl;
     }
     spfom_status st = allreduce(h, acc, acc, (size_t)h->N, kNcclFloat64, kNcclSum);
@@ -488,25 +547,50 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         if (p->tau_mode == 1 && tau[jn] * p->mu > 1.0) { h->err = "params: tau_j * mu must be <= 1"; return bail(SPFOM_EINVAL); }
     }
 
-    // ---- padded quad CSR
+    // ---- length bins; device segment order = (bin, local id), so that every
+    // bin is one contiguous range
+    std::vector<int> segbin(std::max<int64_t>(m, 1));
+    std::vector<int32_t> snew(std::max<int64_t>(m, 1));       // local id -> device slot
+    h->bin_first.assign(kNumBins + 1, 0);
+    {
+        std::vector<int64_t> cnt(kNumBins, 0);
+        for (int64_t i = 0; i < m; ++i) {
+            segbin[i] = bin_of((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
+            cnt[segbin[i]]++;
+        }
+        for (int b = 0; b < kNumBins; ++b) h->bin_first[b + 1] = (int32_t)(h->bin_first[b] + cnt[b]);
+        std::vector<int64_t> fill(h->bin_first.begin(), h->bin_first.end() - 1);
+        h->sorder.assign(std::max<int64_t>(m, 1), 0);
+        for (int64_t i = 0; i < m; ++i) {
+            const int64_t k = fill[segbin[i]]++;
+            h->sorder[k] = (int32_t)i;
+            snew[i] = (int32_t)k;
+        }
+    }
+
+    // ---- padded quad CSR in device order
     std::vector<int32_t> qoff(m + 1, 0);
-    for (int64_t i = 0; i < m; ++i) qoff[i + 1] = qoff[i] + (int32_t)((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
+    for (int64_t k = 0; k < m; ++k) {
+        const int64_t i = h->sorder[k];
+        qoff[k + 1] = qoff[k] + (int32_t)((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
+    }
     const int64_t nq = qoff[m];
     std::vector<int32_t> pidx(4 * std::max<int64_t>(nq, 1), (int32_t)N);
     std::vector<double> vv(4 * std::max<int64_t>(nq, 1), 0.0), om(4 * std::max<int64_t>(nq, 1), 0.0);
-    std::vector<double2> seg(std::max<int64_t>(m, 1));
-    std::vector<double4> warm(std::max<int64_t>(m, 1));
+    std::vector<double2> segc(std::max<int64_t>(m, 1));
+    std::vector<double4> segv(std::max<int64_t>(m, 1));
     h->pos_map.assign(in->nnz, 0);
     bool bad_numeric = false;
 #pragma omp parallel for schedule(dynamic, 4096)
-    for (int64_t i = 0; i < m; ++i) {
-        const int64_t a = in->seg_ptr[i], k = in->seg_ptr[i + 1] - a;
-        std::vector<std::pair<int32_t, int64_t>> order(k);
-        for (int64_t q = 0; q < k; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
+    for (int64_t k = 0; k < m; ++k) {
+        const int64_t i = h->sorder[k];
+        const int64_t a = in->seg_ptr[i], len = in->seg_ptr[i + 1] - a;
+        std::vector<std::pair<int32_t, int64_t>> order(len);
+        for (int64_t q = 0; q < len; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
         std::sort(order.begin(), order.end());
         double vt0 = in->no_purchase[i], svt = 0.0;
-        const int64_t base = 4 * (int64_t)qoff[i];
-        for (int64_t q = 0; q < k; ++q) {
+        const int64_t base = 4 * (int64_t)qoff[k];
+        for (int64_t q = 0; q < len; ++q) {
             const int64_t e = order[q].second;
             const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
             pidx[base + q] = order[q].first;
@@ -516,56 +600,45 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             svt += v - w;
             h->pos_map[e] = base + q;
         }
-        seg[i] = make_double2(in->arrival[i], vt0);
-        // initial projection multipliers (nu, kappa, U)
-        warm[i] = make_double4(0.0, 0.0, in->arrival[i] / (vt0 + svt), 0.0);
+        segc[k] = make_double2(in->arrival[i], vt0);
+        // y0 = lambda and the initial projection multipliers (nu, kappa, U)
+        segv[k] = make_double4(in->arrival[i], 0.0, 0.0, in->arrival[i] / (vt0 + svt));
         if (!std::isfinite(vt0)) bad_numeric = true;
     }
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
 
-    // ---- bins (full sweep lists) and sampled block tables
-    h->bin_first.assign(kNumBins + 1, 0);
-    std::vector<int32_t> binids(std::max<int64_t>(m, 1));
-    {
-        std::vector<int64_t> cnt(kNumBins, 0);
-        std::vector<int> segbin(m);
-        for (int64_t i = 0; i < m; ++i) { segbin[i] = bin_of(qoff[i + 1] - qoff[i]); cnt[segbin[i]]++; }
-        for (int b = 0; b < kNumBins; ++b) h->bin_first[b + 1] = (int32_t)(h->bin_first[b] + cnt[b]);
-        std::vector<int64_t> fill(h->bin_first.begin(), h->bin_first.end() - 1);
-        for (int64_t i = 0; i < m; ++i) binids[fill[segbin[i]]++] = (int32_t)i;
-        std::vector<int32_t> rowoff;
-        std::vector<int32_t> blkids;
-        if (pl.sampled) {
-            const int64_t off = in->segment_offset;
-            rowoff.assign(p->block_iters * (kNumBins + 1), 0);
-            std::vector<std::vector<int32_t>> per(kNumBins);
-            for (int64_t t = 0; t < p->block_iters; ++t) {
-                for (auto &v : per) v.clear();
-                const int32_t *row = p->blocks + t * p->block_size;
-                for (int64_t b = 0; b < p->block_size; ++b) {
-                    const int64_t li = (int64_t)row[b] - off;
-                    if (li >= 0 && li < m) per[segbin[li]].push_back((int32_t)li);
-                }
-                int32_t *ro = rowoff.data() + t * (kNumBins + 1);
-                ro[0] = (int32_t)blkids.size();
-                for (int b = 0; b < kNumBins; ++b) {
-                    blkids.insert(blkids.end(), per[b].begin(), per[b].end());
-                    ro[b + 1] = (int32_t)blkids.size();
-                }
+    // ---- sampled block tables: per (iteration, bin) lists of device slots
+    if (pl.sampled) {
+        std::vector<int32_t> rowoff, blkids;
+        const int64_t off = in->segment_offset;
+        rowoff.assign(p->block_iters * (kNumBins + 1), 0);
+        std::vector<std::vector<int32_t>> per(kNumBins);
+        for (int64_t t = 0; t < p->block_iters; ++t) {
+            for (auto &v : per) v.clear();
+            const int32_t *row = p->blocks + t * p->block_size;
+            for (int64_t b = 0; b < p->block_size; ++b) {
+                const int64_t li = (int64_t)row[b] - off;
+                if (li >= 0 && li < m) per[segbin[li]].push_back(snew[li]);
             }
-            // per-bin max count per row, for static grid sizes
+            int32_t *ro = rowoff.data() + t * (kNumBins + 1);
+            ro[0] = (int32_t)blkids.size();
             for (int b = 0; b < kNumBins; ++b) {
-                int64_t mx = 0;
-                for (int64_t t = 0; t < p->block_iters; ++t) {
-                    const int32_t *ro = rowoff.data() + t * (kNumBins + 1);
-                    mx = std::max<int64_t>(mx, ro[b + 1] - ro[b]);
-                }
-                h->pl.bin_count[b] = mx;
+                blkids.insert(blkids.end(), per[b].begin(), per[b].end());
+                ro[b + 1] = (int32_t)blkids.size();
             }
-            if (!blkids.empty() && cudaMemcpyAsync(slot_ptr<int32_t>(h, O_BLKIDS), blkids.data(), blkids.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D blocks"; return bail(SPFOM_ECUDA); }
-            if (cudaMemcpyAsync(slot_ptr<int32_t>(h, O_ROWOFF), rowoff.data(), rowoff.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D rowoff"; return bail(SPFOM_ECUDA); }
-            if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "sync"; return bail(SPFOM_ECUDA); }
         }
+        // per-bin max count per row, for static grid sizes
+        for (int b = 0; b < kNumBins; ++b) {
+            int64_t mx = 0;
+            for (int64_t t = 0; t < p->block_iters; ++t) {
+                const int32_t *ro = rowoff.data() + t * (kNumBins + 1);
+                mx = std::max<int64_t>(mx, ro[b + 1] - ro[b]);
+            }
+            h->pl.bin_count[b] = mx;
+        }
+        if (!blkids.empty() && cudaMemcpyAsync(slot_ptr<int32_t>(h, O_BLKIDS), blkids.data(), blkids.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D blocks"; return bail(SPFOM_ECUDA); }
+        if (cudaMemcpyAsync(slot_ptr<int32_t>(h, O_ROWOFF), rowoff.data(), rowoff.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D rowoff"; return bail(SPFOM_ECUDA); }
+        if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "sync"; return bail(SPFOM_ECUDA); }
     }
 
     // ---- copies into the workspace
@@ -573,14 +646,14 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         return bytes == 0 || cudaMemcpyAsync(h->ws + h->pl.off[slot], src, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
     };
     std::vector<double> y0(std::max<int64_t>(m, 1));
-    for (int64_t i = 0; i < m; ++i) y0[i] = in->arrival[i];
+    for (int64_t k = 0; k < m; ++k) y0[k] = segv[k].x;
     bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
-              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEG, seg.data(), m * 16) && H2D(O_Y0, y0.data(), m * 8) &&
-              H2D(O_WARM, warm.data(), m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
-              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8) && H2D(O_BINIDS, binids.data(), m * 4);
+              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), m * 16) &&
+              H2D(O_SEGV, segv.data(), m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
+              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8);
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
-    ok = ok && Z(O_Y, nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (N + 1) * 8) && Z(O_SCUR, (N + 1) * 8) &&
+    ok = ok && Z(O_Y, nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
          Z(O_COUNTERS, 64) && Z(O_T, 8);
     if (pl.averaging) ok = ok && Z(O_YBAR, nq * 32) && Z(O_ETABAR, (N + 1) * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
@@ -593,16 +666,20 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.y = slot_ptr<double>(h, O_Y);
     S.ybar = pl.averaging ? slot_ptr<double>(h, O_YBAR) : nullptr;
     S.qoff = slot_ptr<int32_t>(h, O_QOFF);
-    S.seg = slot_ptr<double2>(h, O_SEG);
-    S.y0 = slot_ptr<double>(h, O_Y0);
+    S.segc = slot_ptr<double2>(h, O_SEGC);
+    S.segv = slot_ptr<double4>(h, O_SEGV);
     S.y0bar = pl.averaging ? slot_ptr<double>(h, O_Y0BAR) : nullptr;
-    S.warm = slot_ptr<double4>(h, O_WARM);
     S.r = slot_ptr<double>(h, O_R);
     S.c = slot_ptr<double>(h, O_C);
     S.tau = slot_ptr<double>(h, O_TAU);
     S.eta = slot_ptr<double>(h, O_ETA);
     S.g = slot_ptr<double>(h, O_G);
     S.s = slot_ptr<double>(h, O_ACC);
+    S.spread_off = (int32_t)spread_off(N);
+    S.spread = S.s + S.spread_off;
+    S.spread_n = (int32_t)spread_range(N);
+    S.spread_c = kSpreadCopies;
+    S.fold_in_dual = h->world > 1 ? 0 : 1;
     S.s_prev = slot_ptr<double>(h, O_SCUR);
     S.etabar = pl.averaging ? slot_ptr<double>(h, O_ETABAR) : nullptr;
     S.counters = slot_ptr<unsigned long long>(h, O_COUNTERS);
@@ -666,26 +743,31 @@ spfom_status spfom_usage(spfom_handle *h, double *s) {
     return SPFOM_OK;
 }
 
-static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, double *y, double *y0) {
-    std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1));
+// y0 in device order is either a plain array (pitch 8) or the x field of segv (pitch 32)
+static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, size_t pitch0, double *y,
+                                 double *y0) {
+    std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1)), t0(std::max<int64_t>(h->m, 1));
     if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), dy, h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
-    if (y0 && h->m) CUDA_TRY(h, cudaMemcpyAsync(y0, dy0, h->m * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (y0 && h->m)
+        CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, h->m, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     if (y)
         for (int64_t e = 0; e < h->nnz; ++e) y[e] = tmp[h->pos_map[e]];
+    if (y0)
+        for (int64_t k = 0; k < h->m; ++k) y0[h->sorder[k]] = t0[k];
     return SPFOM_OK;
 }
 
 spfom_status spfom_primal(spfom_handle *h, double *y, double *y0) {
     if (!h) return SPFOM_EINVAL;
-    spfom_status st = fetch_primal(h, h->S.y, h->S.y0, y, y0);
+    spfom_status st = fetch_primal(h, h->S.y, reinterpret_cast<const double *>(h->S.segv), 32, y, y0);
     return st != SPFOM_OK ? st : check_counters(h);
 }
 
 spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double *etabar) {
     if (!h) return SPFOM_EINVAL;
     if (!h->pl.averaging) return fail(h, SPFOM_EINVAL, "averaging is off");
-    spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, ybar, y0bar);
+    spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, 8, ybar, y0bar);
     if (st != SPFOM_OK) return st;
     if (etabar) {
         std::vector<double> tmp(h->N);
@@ -710,7 +792,7 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
         const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];
         if (cnt == 0) continue;
         SegList L{};
-        L.ids = slot_ptr<int32_t>(h, O_BINIDS);
+        L.ids = nullptr;
         L.first = h->bin_first[b];
         L.count = cnt;
         resid_dispatch(b, S, L, pseg + (size_t)b * kResidBlocks * 4, h->stream);
@@ -782,7 +864,13 @@ spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0,
         CUDA_TRY(h, cudaMemcpyAsync(h->S.y, tmp.data(), h->nq * 32, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
-    if (y0) CUDA_TRY(h, cudaMemcpyAsync(h->S.y0, y0, h->m * 8, cudaMemcpyHostToDevice, h->stream));
+    if (y0 && h->m) {
+        std::vector<double> t0(h->m);
+        for (int64_t k = 0; k < h->m; ++k) t0[k] = y0[h->sorder[k]];
+        CUDA_TRY(h, cudaMemcpy2DAsync(reinterpret_cast<double *>(h->S.segv), 32, t0.data(), 8, 8, h->m,
+                                      cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    }
     std::vector<double> t1(h->N + 1, 0.0), t2(h->N + 1, 0.0);
     if (eta) {
         std::vector<double> r(h->N + 1, 0.0);

@@ -15,7 +15,8 @@ constexpr int kPrimalThreads = 128; // K1: 4 warps per block, 4 blocks per SM
 #define SPFOM_PRIMAL_MIN_BLOCKS 3
 #endif
 constexpr int kPrimalMinBlocks = SPFOM_PRIMAL_MIN_BLOCKS;
-constexpr int kHeadMax = 1024;      // products privatised in shared memory (Zipf head, DESIGN.md §K1)
+constexpr int kHeadMax = 1024;      // products privatised in shared memory (Zipf head, DESIGN.md §7)
+constexpr int kGHeadStreamMax = 4096;   // K1 stream: head of g staged in shared memory
 
 struct DevState {
     // per quad (4 padded entries), relabelled product ids, rows sorted by new id
@@ -24,15 +25,21 @@ struct DevState {
     const double *om;     // [4 nq]  omega = w / v (0 on pads)
     double *y;            // [4 nq]  sales iterate
     double *ybar;         // [4 nq]  average (averaging on) or null
-    // per local segment
+    // per local segment (stored in bin order)
     const int32_t *qoff;  // [m+1] quad offsets
-    const double2 *seg;   // [m]   (lambda, vt0 = v0 + sum w)
-    double *y0;           // [m]   no-purchase iterate
+    const double2 *segc;  // [m]   (lambda, vt0 = v0 + sum w), read-only
+    double4 *segv;        // [m]   (y0, nu, kappa, U): no-purchase iterate + warm start of the projection
     double *y0bar;        // [m]   or null
-    double4 *warm;        // [m]   (nu, kappa, U, -) of the last projection
     // per product, N + 1 slots (slot N = dummy of the pads: g = 0)
     const double *r, *c, *tau;
-    double *eta, *g, *s, *s_prev, *etabar;
+    double *eta, *g, *s, *s_prev, *etabar;   // s: usage accumulator (N + 1 slots, then the spread copies)
+    // usage-accumulator copies for the warm part of the Zipf head (stream K1):
+    // products [hh, spread_n) reduce into spread[c * spread_n + j], c = warp % spread_c,
+    // so that no single address takes every segment's update; folded into s
+    // by K3 (world == 1) or k_fold before the allreduce
+    double *spread;                // = s + spread_off
+    int32_t spread_n, spread_c, spread_off;
+    int32_t fold_in_dual;
     // counters (device)
     unsigned long long *counters;  // [0] newton failures, [1] passes
     int64_t *t;                    // completed iterations
@@ -102,6 +109,14 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) 
 }
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
+// fp64 reduction into global memory under a predicate, without a branch
+__device__ __forceinline__ void red_add_if(double *p, double v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p red.global.add.f64 [%0], %1;\n\t}"
+                 :: "l"(p), "d"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void st_v2f64(double *p, double a, double b) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(a), "d"(b) : "memory");
 }
 __device__ __forceinline__ int idx_of(const int4 &q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));

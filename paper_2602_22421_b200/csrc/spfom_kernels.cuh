@@ -21,7 +21,14 @@ namespace spfom {
 __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full) {
     const int64_t t_next = *S.t + 1;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
-        const double sn = full ? S.s[j] : S.s_prev[j] + S.s[j];
+        double acc = S.s[j];
+        if (S.fold_in_dual && j < S.spread_n) {
+            for (int c = 0; c < S.spread_c; ++c) {   // fixed order: deterministic fold of K1's spread copies
+                acc += S.spread[(size_t)c * S.spread_n + j];
+                S.spread[(size_t)c * S.spread_n + j] = 0.0;
+            }
+        }
+        const double sn = full ? acc : S.s_prev[j] + acc;
         const double sx = fma(S.omega_x, sn - S.s_prev[j], sn);
         const double tj = S.tau[j];
         const double e = fmax(0.0, fma(-tj, S.c[j] - sx, (1.0 - tj * S.mu) * S.eta[j]));
@@ -35,6 +42,18 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full) {
 
 __global__ void k_tick(int64_t *t) { *t += 1; }
 
+// world > 1: fold K1's spread copies into the usage accumulator before the allreduce
+__global__ void __launch_bounds__(kThreads) k_fold(DevState S) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S.spread_n) return;
+    double acc = S.s[j];
+    for (int c = 0; c < S.spread_c; ++c) {
+        acc += S.spread[(size_t)c * S.spread_n + j];
+        S.spread[(size_t)c * S.spread_n + j] = 0.0;
+    }
+    S.s[j] = acc;
+}
+
 // a8 averaging of the primal (all rows, so that stale rows count in sampled mode)
 __global__ void __launch_bounds__(kThreads) k_average(DevState S, int64_t nq) {
     const double inv = 1.0 / (double)(*S.t + 1);
@@ -45,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) k_average(DevState S, int64_t nq) {
         st256(S.ybar + 4 * q, ea + (a - ea) * inv, eb + (b - eb) * inv, ec + (c - ec) * inv, ed + (d - ed) * inv);
     }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S.m; i += (int64_t)gridDim.x * blockDim.x)
-        S.y0bar[i] += (S.y0[i] - S.y0bar[i]) * inv;
+        S.y0bar[i] += (S.segv[i].x - S.y0bar[i]) * inv;
 }
 
 // fresh usage: out[j] += sum_i y_ij (out zeroed by the caller); head products
@@ -92,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, d
         double lam = 1.0, vt0 = 1.0, y0 = 1.0;
         int32_t q0 = 0, q1 = 0;
         if (active) {
-            lam = S.seg[i].x; vt0 = S.seg[i].y; y0 = S.y0[i]; q0 = S.qoff[i]; q1 = S.qoff[i + 1];
+            lam = S.segc[i].x; vt0 = S.segc[i].y; y0 = S.segv[i].x; q0 = S.qoff[i]; q1 = S.qoff[i + 1];
         }
         double v[NE], om[NE], y[NE], gj[NE];
 #pragma unroll

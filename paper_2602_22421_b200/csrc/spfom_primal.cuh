@@ -1,4 +1,4 @@
-// spfom_primal.cuh -- K1, the fused primal kernel of one SPFOM iteration.
+// spfom_primal.cuh -- K1, the fused primal kernels of one SPFOM iteration.
 //
 //   a2 gather g_ij = r_j - eta_j (head of g staged in shared memory)
 //   a3 gradient step z_ij = y_ij + theta g_ij, z_i0 = y_i0
@@ -7,14 +7,23 @@
 //      from the segment's previous multipliers; theta = inf: exact inner argmax
 //      by Dinkelbach (reading c6)
 //   a5 usage scatter s_j += y_ij (sampled: y_new - y_old): the Zipf head
-//      j < head goes to per-warp shared-memory histograms, flushed once per
+//      j < HH goes to group-private shared-memory histograms, flushed once per
 //      persistent block; the tail uses global fp64 reductions.
 //
-// Thread mapping: a group of G lanes owns one segment; lane l holds quads
-// l, l+G, .. (Q of them) of the padded row; a quad = 4 entries = one 128-bit
-// id load + three 256-bit loads (v, omega, y).
+// Two kernels share the per-segment device code:
+//   k_primal_stream  full sweep over a contiguous bin (the hot path).  Every
+//                    warp owns a contiguous range of rounds (GPW consecutive
+//                    segments each); a round's rows are contiguous in every
+//                    array, so the warp fetches round r+1 with six TMA bulk
+//                    copies (cp.async.bulk, mbarrier completion) into its
+//                    shared-memory slot while it computes round r.
+//   k_primal         segment lists (sampled blocks, bins longer than 256
+//                    entries): register-direct 128/256-bit loads.
 //
-// KKT system (DESIGN.md §K1): with a_j = z_j - nu + omega_j kappa and the
+// Thread mapping: a group of G lanes owns one segment; lane l holds quads
+// l, l+G, .. (Q of them) of the padded row; a quad = 4 entries.
+//
+// KKT system (DESIGN.md §7): with a_j = z_j - nu + omega_j kappa and the
 // piece C = {a_j >= v_j U} (capped), F = {0 < a_j < v_j U} (free):
 //   R1 = sum_C v_j (a_j - v_j U) - vt0 kappa
 //   R2 = y0 + sum_j omega_j y_j - vt0 U,   R3 = y0 + sum_j y_j - lambda,
@@ -29,14 +38,11 @@
 // re-classifies: if no entry of the group changed class, R is affine on that
 // piece, so the new point solves R = 0 exactly and the segment is done without
 // any reduction.  Otherwise a FULL pass follows at the same point
-// (sufficient-decrease test, backtracking on ||R||_inf).  Every pass also
-// produces y at its point, so the terminating pass yields the output.
+// (sufficient-decrease test, backtracking on ||R||_inf).
 //
-// Head scatter: the warp's segments share one histogram, so their updates of
-// a hot product would collide.  Every lane stages its (id, contribution)
-// pairs in shared memory; then, one segment at a time, all 32 lanes apply
-// that segment's staged updates -- ids within a segment are distinct, so a
-// round has no conflicts and needs no atomics.
+// Head scatter: each G-lane group has its own histogram of the head products
+// (ids are distinct within a segment, so a group's updates never collide and
+// need no atomics); the block sums the histograms once at the end.
 #pragma once
 
 #include "spfom_common.cuh"
@@ -68,11 +74,13 @@ struct PieceSums {
     int nf;
 };
 
-// FULL pass, one entry: classify at (x0, x1, x2) = (nu, kappa, U), accumulate
-// the piece-constant sums, set the class bits, return y_j (branch-free; ptxas
-// turns the selects into FSEL, which beats predicated fp64 here).
-__device__ __forceinline__ double full_entry(double z, double v, double om, double x0, double x1, double x2,
-                                             uint32_t bit, PieceSums &s, uint32_t &cm, uint32_t &fm) {
+// FULL pass, one entry: classify at (x0, x1, x2) = (nu, kappa, U), set the
+// class bits and accumulate the piece-constant sums.  Branch-free: the inputs
+// are selected (3 fp64 selects) and the 8 sums are plain fp64 adds -- ptxas
+// if-converts predicated fp64 into selects of the results, which costs more.
+// |F| is popc(fm) after the entry loop.
+__device__ __forceinline__ void full_entry(double z, double v, double om, double x0, double x1, double x2,
+                                           uint32_t bit, PieceSums &s, uint32_t &cm, uint32_t &fm) {
     const double a = fma(om, x1, z - x0);     // a = omega kappa + (z - nu)
     const double cap = v * x2;                // v U
     const bool isC = a >= cap;
@@ -90,85 +98,552 @@ __device__ __forceinline__ double full_entry(double z, double v, double om, doub
     s.sfwa = fma(om, af, s.sfwa);             // sum_F omega a
     s.fw += wf;                               // sum_F omega
     s.fww = fma(wf, om, s.fww);               // sum_F omega^2
-    s.nf += isF ? 1 : 0;
-    return isC ? cap : af;
 }
 
-// CHECK pass, one entry: class bits and y_j at (x0, x1, x2) only.
-__device__ __forceinline__ double check_entry(double z, double v, double om, double x0, double x1, double x2,
-                                              uint32_t bit, uint32_t &cm, uint32_t &fm) {
+// CHECK pass, one entry: class bits at (x0, x1, x2) only.
+__device__ __forceinline__ void check_bits(double z, double v, double om, double x0, double x1, double x2,
+                                           uint32_t bit, uint32_t &cm, uint32_t &fm) {
     const double a = fma(om, x1, z - x0);
     const double cap = v * x2;
-    const bool isC = a >= cap;
-    const bool isF = !isC && (a > 0.0);
-    cm |= isC ? bit : 0u;
-    fm |= isF ? bit : 0u;
-    return isC ? cap : (isF ? a : 0.0);
+    asm("{\n\t.reg .pred pc, pf;\n\t"
+        "setp.ge.f64 pc, %2, %3;\n\t"
+        "setp.gt.and.f64 pf, %2, 0d0000000000000000, !pc;\n\t"
+        "@pc or.b32 %0, %0, %4;\n\t"
+        "@pf or.b32 %1, %1, %4;\n\t"
+        "}"
+        : "+r"(cm), "+r"(fm)
+        : "d"(a), "d"(cap), "r"(bit));
 }
 
-template <int Q>
-struct PrimalSmem {
-    static constexpr int WARPS = kPrimalThreads / 32;
-    static constexpr int NE = 4 * Q;
-    double hist[WARPS][kHeadMax];          // per-warp usage of the head products
-    double ghead[kHeadMax];                // price vector g on the head products
-    double stage_val[WARPS][32 * NE];      // staged head contributions, [warp][e * 32 + lane]
-    int stage_idx[WARPS][32 * NE];
+// Output, one entry: y_j = clamp(a_j, 0, v_j U) at (x0, x1, x2).
+__device__ __forceinline__ double y_entry(double z, double v, double om, double x0, double x1, double x2) {
+    const double a = fma(om, x1, z - x0);
+    const double cap = v * x2;
+    double y;
+    // explicit selects (the C form is pattern-matched into a NaN-aware fmax)
+    asm("{\n\t.reg .pred pc, pp;\n\t.reg .f64 t;\n\t"
+        "setp.ge.f64 pc, %1, %2;\n\t"
+        "setp.gt.f64 pp, %1, 0d0000000000000000;\n\t"
+        "selp.f64 t, %1, 0d0000000000000000, pp;\n\t"
+        "selp.f64 %0, %2, t, pc;\n\t}"
+        : "=d"(y) : "d"(a), "d"(cap));
+    return y;
+}
+
+struct ProjStats {
+    unsigned long long passes = 0, failures = 0, restarts = 0;
 };
 
-// Resident blocks per SM the register budget targets: one quad per lane fits 4
-// blocks (128 registers), wider lanes 3.
-template <int Q>
-constexpr int primal_min_blocks() { return kPrimalMinBlocks; }
+// a4, theta < inf: Euclidean projection of (z0, z) onto Y_i for the segment of
+// this G-lane group (reading c5).  (x0, x1, x2) holds the warm
+// start (nu, kappa, U) on entry and the final multipliers on exit; yv / y0new
+// receive the projected point.  Must be called by the whole warp.
+template <int G, int NE>
+__device__ __forceinline__ void project_group(const double (&z)[NE], const double (&v)[NE], const double (&om)[NE],
+                                              double z0, double lam, double vt0, bool active, unsigned gmask,
+                                              int max_newton, double &x0, double &x1, double &x2,
+                                              double (&yv)[NE], double &y0new, ProjStats &st) {
+    double sabs = 0.0;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) sabs += fabs(z[e]);
+    sabs = group_sum<G>(sabs);
+    const double tol = 1e-13 * (lam + fabs(z0) + sabs) * fmax(1.0, vt0);
+
+    double a0 = x0, a1 = x1, a2 = x2;                   // last accepted point
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, step = 1.0, Ra = 0.0;
+    uint32_t cA = 0, fA = 0;                            // class bitmasks at the accepted point
+    bool go = active, full = true, first = true, failed = false, restarted = false;
+    int passes = 0;
+    const int restart_at = max_newton / 2;
+    while (__any_sync(0xffffffffu, go)) {
+        // safeguard: a segment still unconverged after half the budget restarts
+        // from the cold point (nu, kappa, U) = ((z0 + sum z - lam)/(k+1), 0, lam/(vt0 + sum vt))
+        if (__any_sync(0xffffffffu, go && passes == restart_at)) {
+            double sz = 0.0, svt = 0.0, nk = 0.0;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                sz += z[e];
+                svt += fma(-v[e], om[e], v[e]);
+                nk += v[e] > 0.0 ? 1.0 : 0.0;
+            }
+            sz = group_sum<G>(sz);
+            svt = group_sum<G>(svt);
+            nk = group_sum<G>(nk);
+            if (go && passes == restart_at) {
+                x0 = (z0 + sz - lam) / (nk + 1.0);
+                x1 = 0.0;
+                x2 = lam / (vt0 + svt);
+                full = true;
+                first = true;
+                step = 1.0;
+                restarted = true;
+            }
+        }
+        const bool need = __any_sync(0xffffffffu, go && full);   // warp-uniform
+        uint32_t cm = 0, fm = 0;
+        if (!need) {
+            // CHECK pass for every unfinished group of the warp
+#pragma unroll
+            for (int e = 0; e < NE; ++e) check_bits(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
+            const bool changed = (__ballot_sync(0xffffffffu, (cm != cA) || (fm != fA)) & gmask) != 0u;
+            if (go) {
+                ++passes;
+                if (!changed) go = false;     // same piece: R(x) = 0 exactly
+                else full = true;             // piece moved: evaluate R, J here
+            }
+            continue;
+        }
+        PieceSums ps = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
+#pragma unroll
+        for (int e = 0; e < NE; ++e) full_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, ps, cm, fm);
+        ps.nf = __popc(fm);
+        ps.sfa = group_sum<G>(ps.sfa);   ps.sfwa = group_sum<G>(ps.sfwa);
+        ps.rva = group_sum<G>(ps.rva);   ps.cv = group_sum<G>(ps.cv);
+        ps.cvw = group_sum<G>(ps.cvw);   ps.cvv = group_sum<G>(ps.cvv);
+        ps.fw = group_sum<G>(ps.fw);     ps.fww = group_sum<G>(ps.fww);
+#pragma unroll
+        for (int o = G / 2; o >= 1; o >>= 1) ps.nf += __shfl_xor_sync(0xffffffffu, ps.nf, o);
+        const bool changed = (__ballot_sync(0xffffffffu, (cm != cA) || (fm != fA)) & gmask) != 0u;
+        if (go) {
+            ++passes;
+            if (!full) {
+                // CHECK pass (evaluated as a full pass because another group needed one)
+                if (!changed) go = false;
+                else full = true;
+            } else {
+                const double y0c = z0 - x0 + x1;
+                const double sy = fma(x2, ps.cv, ps.sfa);
+                const double swy = fma(x2, ps.cvw, ps.sfwa);
+                const double r1 = fma(-x2, ps.cvv, ps.rva);
+                const double R[3] = {r1 - vt0 * x1, y0c + swy - vt0 * x2, y0c + sy - lam};
+                const double nr = fmax(fabs(R[0]), fmax(fabs(R[1]), fabs(R[2])));
+                bool done = !(nr > tol);
+                if (!isfinite(nr)) { done = true; failed = true; }
+                if (!done) {
+                    if (first || nr <= (1.0 - 1e-4 * step) * Ra) {
+                        const double dnf = (double)ps.nf;
+                        const double J[3][3] = {{-ps.cv, ps.cvw - vt0, -ps.cvv},
+                                                {-1.0 - ps.fw, 1.0 + ps.fww, ps.cvw - vt0},
+                                                {-1.0 - dnf, 1.0 + ps.fw, ps.cv}};
+                        double d[3];
+                        if (!newton_dir(J, R, d)) {
+                            done = true;
+                            failed = true;
+                        } else {
+                            a0 = x0; a1 = x1; a2 = x2;
+                            d0 = d[0]; d1 = d[1]; d2 = d[2];
+                            Ra = nr;
+                            cA = cm;
+                            fA = fm;
+                            step = 1.0;
+                            full = false;
+                        }
+                    } else {
+                        step *= 0.5;
+                        full = true;
+                        if (step < 1e-12) { done = true; failed = true; }
+                    }
+                    if (!done && passes >= max_newton) {
+                        done = true;                  // budget spent: keep the last evaluated point
+                        failed = true;
+                    }
+                    if (!done) {
+                        x0 = a0 + step * d0;
+                        x1 = a1 + step * d1;
+                        x2 = a2 + step * d2;
+                        first = false;
+                    }
+                }
+                if (done) go = false;
+            }
+        }
+    }
+    if (active && (threadIdx.x & (G - 1)) == 0) {
+        st.passes += (unsigned long long)passes;
+        st.failures += failed ? 1ull : 0ull;
+        st.restarts += restarted ? 1ull : 0ull;
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) yv[e] = y_entry(z[e], v[e], om[e], x0, x1, x2);
+    y0new = z0 - x0 + x1;
+}
+
+// a4, theta = inf: exact inner argmax by Dinkelbach from z = 0 (reading c6;
+// SURVEY App. A.3).  g holds the prices g_ij of the group's entries.
+template <int G, int NE>
+__device__ __forceinline__ void argmax_group(const double (&g)[NE], const double (&v)[NE], const double (&om)[NE],
+                                             double lam, double vt0, bool active, double (&yv)[NE],
+                                             double &y0new) {
+    double zs = 0.0, den = 0.0, sv_in = 0.0;
+    bool go = active;
+    for (int it = 0; it < 64; ++it) {
+        double num = 0.0, dd = 0.0, sv = 0.0;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const double gv = g[e] * v[e], vt = fma(-v[e], om[e], v[e]);
+            const bool in = gv > zs * vt;
+            num += in ? gv : 0.0;
+            dd += in ? vt : 0.0;
+            sv += in ? v[e] : 0.0;
+        }
+        num = group_sum<G>(num);
+        dd = group_sum<G>(dd);
+        sv = group_sum<G>(sv);
+        den = dd;
+        sv_in = sv;
+        const double zn = num / (vt0 + dd);
+        const bool more = go && (zn > zs);
+        if (more) zs = zn;
+        go = more;
+        if (!__any_sync(0xffffffffu, go)) break;
+    }
+    const double U = lam / (vt0 + den);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) yv[e] = (g[e] * v[e] > zs * fma(-v[e], om[e], v[e])) ? v[e] * U : 0.0;
+    y0new = lam - U * sv_in;
+}
+
+// a5, one group: head entries into the group's private histogram, tail
+// entries (and no pads: pads carry id N) into s by fp64 reductions.
+template <int NE>
+__device__ __forceinline__ void scatter_group(const int (&idx)[NE], const double (&c)[NE], double *hg, int HH,
+                                              double *s, int N) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const int j = idx[e];
+        if (j < HH) hg[j] += c[e];
+        red_add_if(s + j, c[e], j >= HH && j < N);
+    }
+}
+
+// Block-wide flush of the group histograms (nh of them, stride hs doubles).
+__device__ __forceinline__ void flush_hists(const double *hist, int nh, int hs, int HH, int N, double *s) {
+    const int lim = HH < N ? HH : N;
+    for (int j = threadIdx.x; j < lim; j += blockDim.x) {
+        double sum = 0.0;
+        for (int h = 0; h < nh; ++h) sum += hist[h * hs + j];
+        if (sum != 0.0) atomicAdd(s + j, sum);
+    }
+}
+
+// group histogram stride: HH + 1 doubles, so that the same product of two
+// groups falls in different banks
+__host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
+
+// ============================================================== k_primal_stream
+// Full sweep over segments [first, first + count) of one bin (contiguous).
+#ifndef SPFOM_WARP_HIST
+#define SPFOM_WARP_HIST 0
+#endif
+#ifndef SPFOM_SPREAD_C
+#define SPFOM_SPREAD_C 8
+#endif
+template <int G, int Q>
+struct StreamLayout {
+    static constexpr int GPW = 32 / G;                 // segments per round (per warp)
+    static constexpr int QMAX = GPW * G * Q;           // quads per round, at most
+    static constexpr int QW = ((GPW + 8) + 3) & ~3;    // qoff window of the next round (ints)
+    static constexpr uint32_t OFF_SEGV = 0;                            // double4 x GPW
+    static constexpr uint32_t OFF_SEGC = 32u * GPW;                    // double2 x GPW
+    static constexpr uint32_t OFF_QW = OFF_SEGC + 16u * GPW;           // int x QW
+    // quad arrays hold QMAX + 1 quads: index QMAX is an inert zero quad (id N,
+    // v = omega = y = 0) that lanes without a quad read instead of branching
+    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u) & ~63u;    // double4 x (QMAX + 1)
+    static constexpr uint32_t OFF_OM = OFF_V + 32u * (QMAX + 1);           // double4 x (QMAX + 1)
+    static constexpr uint32_t OFF_Y = OFF_OM + 32u * (QMAX + 1);           // double4 x (QMAX + 1)
+    static constexpr uint32_t OFF_IDS = OFF_Y + 32u * (QMAX + 1);          // int4 x (QMAX + 1)
+    static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
+    // head products per histogram: one per group (GPW of them) or one per warp
+    static constexpr int NHIST = SPFOM_WARP_HIST ? 1 : GPW;
+    static constexpr int HH = 1024 / NHIST;
+    static constexpr uint32_t HIST = (uint32_t)NHIST * hist_stride(HH) * 8u;   // bytes per warp
+    static constexpr uint32_t PER_WARP = SLOT + ((HIST + 127u) & ~127u);
+};
+
+constexpr int kStreamWarps = 12;            // one persistent block of 12 warps per SM (168 registers)
+constexpr int kStreamThreads = 32 * kStreamWarps;
+
+struct StreamList {
+    int64_t first, count;   // segments [first, first + count), all of one bin
+    int32_t ghead;          // g staged in shared memory for products [0, ghead)
+    int32_t hh;             // group histograms cover products [0, hh) (<= Layout::HH)
+};
+
+template <int G, int Q>
+__host__ __device__ constexpr size_t stream_smem_fixed() {
+    return (size_t)kStreamWarps * StreamLayout<G, Q>::PER_WARP + 128;   // + mbarriers
+}
+
+template <int G, int Q, bool ARGMAX>
+__global__ void __launch_bounds__(kStreamThreads, 1) k_primal_stream(DevState S, StreamList L) {
+    using LY = StreamLayout<G, Q>;
+    constexpr int NE = 4 * Q;
+    constexpr int GPW = LY::GPW;
+    static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
+    static_assert(GPW + 1 <= 32, "qoff lanes");
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const int gidx = lane / G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gidx * G));
+    const int N = (int)S.N;
+    const int HG = L.ghead, HH = L.hh;
+    constexpr int HS = hist_stride(LY::HH);
+
+    unsigned char *slot = smem + (size_t)warp * LY::PER_WARP;
+    double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)kStreamWarps * LY::PER_WARP) + warp;
+    double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q>());
+    double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) +
+                 (LY::NHIST > 1 ? gidx * HS : 0);
+    const int spread_n = S.spread_n;
+    const int spread_rel = S.spread_off + ((blockIdx.x * kStreamWarps + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
+
+    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
+    for (int w = 0; w < kStreamWarps; ++w) {
+        double *h = reinterpret_cast<double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
+        for (int j = threadIdx.x; j < LY::NHIST * HS; j += blockDim.x) h[j] = 0.0;
+    }
+    if (lane < 6) {   // this warp's inert zero quad
+        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[lane] = 0.0;
+        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[lane] = 0.0;
+        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[lane] = 0.0;
+        if (lane < 4) reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[lane] = N;
+    }
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    (void)hist_all;
+
+    // this warp's rounds [r0, r1) of GPW consecutive segments
+    const int64_t rounds = (L.count + GPW - 1) / GPW;
+    const int64_t W = (int64_t)gridDim.x * kStreamWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kStreamWarps + warp;
+    const int64_t r0 = rounds * gw / W, r1 = rounds * (gw + 1) / W;
+
+    // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
+    auto qload = [&](int64_t r) -> int32_t {
+        int64_t k = GPW * r + (lane < GPW ? lane : GPW);
+        k = k < L.count ? k : L.count;
+        return S.qoff[L.first + k];
+    };
+    // lanes 0..6 issue the bulk copies of round r (q: this lane's qoff of round r):
+    // segment state, quads, and (when the warp has a round r + 1) the 16-B
+    // aligned qoff window that holds round r + 1's offsets
+    auto issue = [&](int64_t r, int32_t q) {
+        const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
+        const int64_t s0 = L.first + GPW * r;
+        const int64_t left = L.count - GPW * r;
+        const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
+        const uint32_t nq = (uint32_t)(qb - qa);
+        const int64_t w0 = (s0 + GPW) & ~(int64_t)3;                  // window of round r + 1
+        const uint32_t wbytes = (r + 1 < r1) ? 4u * LY::QW : 0u;
+        // one elected lane, straight-line: the copies take uniform operands
+        if (lane == 0) {
+            mbar_arrive_expect_tx(bar, 48u * n + 112u * nq + wbytes);
+            bulk_g2s(slot + LY::OFF_SEGV, S.segv + s0, 32u * n, bar);
+            bulk_g2s(slot + LY::OFF_SEGC, S.segc + s0, 16u * n, bar);
+            if (wbytes) bulk_g2s(slot + LY::OFF_QW, S.qoff + w0, wbytes, bar);
+            if (nq > 0) {
+                bulk_g2s(slot + LY::OFF_IDS, S.pidx + qa, 16u * nq, bar);
+                bulk_g2s(slot + LY::OFF_V, S.v + 4 * (int64_t)qa, 32u * nq, bar);
+                bulk_g2s(slot + LY::OFF_OM, S.om + 4 * (int64_t)qa, 32u * nq, bar);
+                bulk_g2s(slot + LY::OFF_Y, S.y + 4 * (int64_t)qa, 32u * nq, bar);
+            }
+        }
+    };
+
+    ProjStats st;
+    int32_t qc = 0;
+    if (r0 < r1) {
+        qc = qload(r0);
+        issue(r0, qc);
+    }
+    for (int64_t r = r0; r < r1; ++r) {
+        mbar_wait(bar, (uint32_t)((r - r0) & 1));
+        // round r + 1's offsets from the window that arrived with this round
+        int32_t qn = 0;
+        if (r + 1 < r1) {
+            const int64_t s1 = L.first + GPW * (r + 1);
+            int64_t k = GPW * (r + 1) + (lane < GPW ? lane : GPW);
+            k = k < L.count ? k : L.count;
+            qn = reinterpret_cast<const int32_t *>(slot + LY::OFF_QW)[L.first + k - (s1 & ~(int64_t)3)];
+        }
+        const int32_t base = __shfl_sync(0xffffffffu, qc, 0);
+        const int32_t qa = __shfl_sync(0xffffffffu, qc, gidx);
+        const int32_t qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
+        const int64_t left = L.count - GPW * r;
+        const bool active = gidx < left;
+        const int64_t i = L.first + GPW * r + gidx;
+
+        // ---- segment state and this lane's quads, from the slot
+        double lam = 1.0, vt0 = 1.0;
+        double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
+        if (active) {
+            sv = reinterpret_cast<const double4 *>(slot + LY::OFF_SEGV)[gidx];
+            const double2 sc = reinterpret_cast<const double2 *>(slot + LY::OFF_SEGC)[gidx];
+            lam = sc.x;
+            vt0 = sc.y;
+        }
+        const double z0 = sv.x;
+        int idx[NE];
+        double v[NE], om[NE], z[NE];
+#pragma unroll
+        for (int t = 0; t < Q; ++t) {
+            const int32_t q = qa + gl + G * t;
+            const int p = q < qb ? q - base : LY::QMAX;          // no quad: the inert zero quad
+            const int4 id4 = reinterpret_cast<const int4 *>(slot + LY::OFF_IDS)[p];
+            idx[4 * t + 0] = id4.x; idx[4 * t + 1] = id4.y; idx[4 * t + 2] = id4.z; idx[4 * t + 3] = id4.w;
+            const double2 *vp = reinterpret_cast<const double2 *>(slot + LY::OFF_V) + 2 * p;
+            const double2 *wp = reinterpret_cast<const double2 *>(slot + LY::OFF_OM) + 2 * p;
+            const double2 *yp = reinterpret_cast<const double2 *>(slot + LY::OFF_Y) + 2 * p;
+            const double2 v01 = vp[0], v23 = vp[1], w01 = wp[0], w23 = wp[1], y01 = yp[0], y23 = yp[1];
+            v[4 * t + 0] = v01.x; v[4 * t + 1] = v01.y; v[4 * t + 2] = v23.x; v[4 * t + 3] = v23.y;
+            om[4 * t + 0] = w01.x; om[4 * t + 1] = w01.y; om[4 * t + 2] = w23.x; om[4 * t + 3] = w23.y;
+            z[4 * t + 0] = y01.x; z[4 * t + 1] = y01.y; z[4 * t + 2] = y23.x; z[4 * t + 3] = y23.y;
+        }
+        // the slot is free: fetch round r + 1 into it while this round computes
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (r + 1 < r1) issue(r + 1, qn);
+
+        // a2: price gather (g[N] = 0 for pads; head from shared memory)
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int j = idx[e];
+            const double gj = (j < HG) ? ghead[j] : __ldg(S.g + j);
+            if constexpr (ARGMAX) z[e] = gj;             // theta = inf: keep g itself
+            else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
+        }
+
+        double yv[NE];
+        double y0new;
+        double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+        if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
+        else project_group<G, NE>(z, v, om, z0, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
+
+        // ---- write back (y, segment state), a5 usage scatter
+#pragma unroll
+        for (int t = 0; t < Q; ++t) {
+            const int32_t q = qa + gl + G * t;
+            if (q < qb) st256(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
+        }
+        if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+        // a5: head -> histogram, warm head -> spread copies, tail -> s
+        if constexpr (LY::NHIST > 1) {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int j = idx[e];
+                if (j < HH) hg[j] += yv[e];
+            }
+        } else {
+#pragma unroll
+            for (int gg = 0; gg < GPW; ++gg) {
+                if (gidx == gg) {
+#pragma unroll
+                    for (int e = 0; e < NE; ++e) {
+                        const int j = idx[e];
+                        if (j < HH) hg[j] += yv[e];
+                    }
+                }
+                __syncwarp();
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int j = idx[e];
+            const int off = j < spread_n ? spread_rel + j : j;     // warm head -> this warp's spread copy
+            red_add_if(S.s + off, yv[e], j >= HH && j < N);
+        }
+        qc = qn;
+    }
+    if constexpr (!ARGMAX) {
+        if (st.passes) {
+            atomicAdd(S.counters + 1, st.passes);
+            if (st.failures) atomicAdd(S.counters + 0, st.failures);
+            if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
+        }
+    }
+    __syncthreads();
+    // flush: histogram h of warp w lives at w * PER_WARP + SLOT + h * HS
+    {
+        const int lim = HH < N ? HH : N;
+        for (int j = threadIdx.x; j < lim; j += blockDim.x) {
+            double sum = 0.0;
+            for (int w = 0; w < kStreamWarps; ++w) {
+                const double *h = reinterpret_cast<const double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
+#pragma unroll
+                for (int g2 = 0; g2 < LY::NHIST; ++g2) sum += h[g2 * HS + j];
+            }
+            if (sum != 0.0) atomicAdd(S.s + j, sum);
+        }
+    }
+}
+
+// ============================================================== k_primal (lists)
+// Segments from a list (sampled blocks) or long-row bins: register-direct loads.
+template <int Q, int G>
+struct ListSmem {
+    static constexpr int WARPS = kPrimalThreads / 32;
+    static constexpr int GPW = 32 / G;
+    static constexpr int HH = 1024 / GPW;
+    double hist[WARPS * GPW * hist_stride(HH)];   // group histograms of the head products
+    double ghead[kHeadMax];                       // price vector g on the head products
+};
 
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
-__global__ void __launch_bounds__(kPrimalThreads, primal_min_blocks<Q>()) k_primal(DevState S, SegList L) {
+__global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(DevState S, SegList L) {
+    using SM = ListSmem<Q, G>;
     constexpr int NE = 4 * Q;               // entries per lane
     constexpr int GPW = 32 / G;             // segments per warp
     constexpr int WARPS = kPrimalThreads / 32;
+    constexpr int HS = hist_stride(SM::HH);
     static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    PrimalSmem<Q> &sm = *reinterpret_cast<PrimalSmem<Q> *>(smem_raw);
+    SM &sm = *reinterpret_cast<SM *>(smem_raw);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const int gidx = lane / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gidx * G));
-    const int H = L.head;
+    const int N = (int)S.N;
+    const int H = L.head;                    // ghead and histogram coverage
+    const int HH = H < SM::HH ? H : SM::HH;
 
-    for (int j = threadIdx.x; j < H; j += kPrimalThreads) {
-        sm.ghead[j] = S.g[j];
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) sm.hist[w][j] = 0.0;
-    }
+    for (int j = threadIdx.x; j < H; j += kPrimalThreads) sm.ghead[j] = S.g[j];
+    for (int j = threadIdx.x; j < WARPS * GPW * HS; j += kPrimalThreads) sm.hist[j] = 0.0;
     __syncthreads();
-    double *hw = sm.hist[warp];
-    double *stv = sm.stage_val[warp];
-    int *sti = sm.stage_idx[warp];
+    double *hg = sm.hist + (warp * GPW + gidx) * HS;
 
     const int64_t groups_per_block = kPrimalThreads / G;
     const int64_t total = seg_count(L, S);
     const int64_t stride = (int64_t)gridDim.x * groups_per_block;
     const int64_t slot_end = ((total + stride - 1) / stride) * stride;   // warp-uniform trip count
-    unsigned long long passes_acc = 0, fail_acc = 0, restart_acc = 0;
+    ProjStats st;
 
     for (int64_t slot = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; slot < slot_end; slot += stride) {
         int64_t i = 0;
         const bool active = seg_slot(L, S, slot, i);
 
-        // ---- segment scalars and this lane's quads
-        double lam = 1.0, vt0 = 1.0, z0 = 1.0;
+        // ---- segment state and this lane's quads
+        double lam = 1.0, vt0 = 1.0;
+        double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
         int32_t q0 = 0, q1 = 0;
         if (active) {
-            const double2 sv = S.seg[i];
-            lam = sv.x;
-            vt0 = sv.y;
-            z0 = S.y0[i];
+            const double2 sc = S.segc[i];
+            lam = sc.x;
+            vt0 = sc.y;
+            sv = S.segv[i];
             q0 = S.qoff[i];
             q1 = S.qoff[i + 1];
         }
+        const double z0 = sv.x;
         int idx[NE];
         double v[NE], om[NE], z[NE];
         double yold[SAMPLED ? NE : 1];
@@ -185,7 +660,7 @@ __global__ void __launch_bounds__(kPrimalThreads, primal_min_blocks<Q>()) k_prim
             } else {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    idx[4 * t + e] = (int)S.N;
+                    idx[4 * t + e] = N;
                     v[4 * t + e] = 0.0;
                     om[4 * t + e] = 0.0;
                 }
@@ -205,207 +680,34 @@ __global__ void __launch_bounds__(kPrimalThreads, primal_min_blocks<Q>()) k_prim
             else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
         }
 
-        double yv[NE];                          // y at the terminating point
+        double yv[NE];
         double y0new;
-        if constexpr (ARGMAX) {
-            // ---- exact inner argmax, Dinkelbach from z = 0 (reading c6)
-            double zs = 0.0, den = 0.0, sv_in = 0.0;
-            bool go = active;
-            for (int it = 0; it < 64; ++it) {
-                double num = 0.0, dd = 0.0, sv = 0.0;
-#pragma unroll
-                for (int e = 0; e < NE; ++e) {
-                    const double gv = z[e] * v[e], vt = fma(-v[e], om[e], v[e]);
-                    const bool in = gv > zs * vt;
-                    num += in ? gv : 0.0;
-                    dd += in ? vt : 0.0;
-                    sv += in ? v[e] : 0.0;
-                }
-                num = group_sum<G>(num);
-                dd = group_sum<G>(dd);
-                sv = group_sum<G>(sv);
-                den = dd;
-                sv_in = sv;
-                const double zn = num / (vt0 + dd);
-                const bool more = go && (zn > zs);
-                if (more) zs = zn;
-                go = more;
-                if (!__any_sync(0xffffffffu, go)) break;
-            }
-            const double U = lam / (vt0 + den);
-#pragma unroll
-            for (int e = 0; e < NE; ++e) yv[e] = (z[e] * v[e] > zs * fma(-v[e], om[e], v[e])) ? v[e] * U : 0.0;
-            y0new = lam - U * sv_in;
-        } else {
-            double sabs = 0.0;
-#pragma unroll
-            for (int e = 0; e < NE; ++e) sabs += fabs(z[e]);
-            sabs = group_sum<G>(sabs);
-            const double tol = 1e-13 * (lam + fabs(z0) + sabs) * fmax(1.0, vt0);
+        double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+        if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
+        else project_group<G, NE>(z, v, om, z0, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
 
-            const double4 wm = active ? S.warm[i] : make_double4(0.0, 0.0, 1.0, 0.0);
-            double x0 = wm.x, x1 = wm.y, x2 = wm.z;             // trial point (nu, kappa, U)
-            double a0 = x0, a1 = x1, a2 = x2;                   // last accepted point
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0, step = 1.0, Ra = 0.0;
-            uint32_t cA = 0, fA = 0;                            // class bitmasks at the accepted point
-            bool go = active, full = true, first = true, failed = false, restarted = false;
-            int passes = 0;
-            const int restart_at = S.max_newton / 2;
-            while (__any_sync(0xffffffffu, go)) {
-                // safeguard: a segment still unconverged after half the budget restarts
-                // from the cold point (nu, kappa, U) = ((z0 + sum z - lam)/(k+1), 0, lam/(vt0 + sum vt))
-                if (__any_sync(0xffffffffu, go && passes == restart_at)) {
-                    double sz = 0.0, svt = 0.0, nk = 0.0;
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) {
-                        sz += z[e];
-                        svt += fma(-v[e], om[e], v[e]);
-                        nk += v[e] > 0.0 ? 1.0 : 0.0;
-                    }
-                    sz = group_sum<G>(sz);
-                    svt = group_sum<G>(svt);
-                    nk = group_sum<G>(nk);
-                    if (go && passes == restart_at) {
-                        x0 = (z0 + sz - lam) / (nk + 1.0);
-                        x1 = 0.0;
-                        x2 = lam / (vt0 + svt);
-                        full = true;
-                        first = true;
-                        step = 1.0;
-                        restarted = true;
-                    }
-                }
-                const bool need = __any_sync(0xffffffffu, go && full);   // warp-uniform
-                uint32_t cm = 0, fm = 0;
-                PieceSums ps = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0};
-                if (need) {
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) (void)full_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, ps, cm, fm);
-                    ps.sfa = group_sum<G>(ps.sfa);   ps.sfwa = group_sum<G>(ps.sfwa);
-                    ps.rva = group_sum<G>(ps.rva);   ps.cv = group_sum<G>(ps.cv);
-                    ps.cvw = group_sum<G>(ps.cvw);   ps.cvv = group_sum<G>(ps.cvv);
-                    ps.fw = group_sum<G>(ps.fw);     ps.fww = group_sum<G>(ps.fww);
-#pragma unroll
-                    for (int o = G / 2; o >= 1; o >>= 1) ps.nf += __shfl_xor_sync(0xffffffffu, ps.nf, o);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) (void)check_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
-                }
-                const bool changed = (__ballot_sync(0xffffffffu, (cm != cA) || (fm != fA)) & gmask) != 0u;
-                if (go) {
-                    ++passes;
-                    if (!full) {
-                        // CHECK pass after a full Newton step from the accepted point
-                        if (!changed) go = false;     // same piece: R(x) = 0 exactly
-                        else full = true;             // piece moved: evaluate R, J here
-                    } else {
-                        const double y0c = z0 - x0 + x1;
-                        const double sy = fma(x2, ps.cv, ps.sfa);
-                        const double swy = fma(x2, ps.cvw, ps.sfwa);
-                        const double r1 = fma(-x2, ps.cvv, ps.rva);
-                        const double R[3] = {r1 - vt0 * x1, y0c + swy - vt0 * x2, y0c + sy - lam};
-                        const double nr = fmax(fabs(R[0]), fmax(fabs(R[1]), fabs(R[2])));
-                        bool done = !(nr > tol);
-                        if (!isfinite(nr)) { done = true; failed = true; }
-                        if (!done) {
-                            if (first || nr <= (1.0 - 1e-4 * step) * Ra) {
-                                const double dnf = (double)ps.nf;
-                                const double J[3][3] = {{-ps.cv, ps.cvw - vt0, -ps.cvv},
-                                                        {-1.0 - ps.fw, 1.0 + ps.fww, ps.cvw - vt0},
-                                                        {-1.0 - dnf, 1.0 + ps.fw, ps.cv}};
-                                double d[3];
-                                if (!newton_dir(J, R, d)) {
-                                    done = true;
-                                    failed = true;
-                                } else {
-                                    a0 = x0; a1 = x1; a2 = x2;
-                                    d0 = d[0]; d1 = d[1]; d2 = d[2];
-                                    Ra = nr;
-                                    cA = cm;
-                                    fA = fm;
-                                    step = 1.0;
-                                    full = false;
-                                }
-                            } else {
-                                step *= 0.5;
-                                full = true;
-                                if (step < 1e-12) { done = true; failed = true; }
-                            }
-                            if (!done && passes >= S.max_newton) {
-                                // budget spent: keep the last evaluated point
-                                done = true;
-                                failed = true;
-                            }
-                            if (!done) {
-                                x0 = a0 + step * d0;
-                                x1 = a1 + step * d1;
-                                x2 = a2 + step * d2;
-                                first = false;
-                            }
-                        }
-                        if (done) go = false;
-                    }
-                }
-            }
-            if (active && gl == 0) {
-                passes_acc += (unsigned long long)passes;
-                fail_acc += failed ? 1ull : 0ull;
-                restart_acc += restarted ? 1ull : 0ull;
-                S.warm[i] = make_double4(x0, x1, x2, 0.0);
-            }
-            uint32_t cm = 0, fm = 0;
-#pragma unroll
-            for (int e = 0; e < NE; ++e) yv[e] = check_entry(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
-            y0new = z0 - x0 + x1;
-        }
-
-        // ---- write back, a5 usage scatter (tail: global RED; head: staged)
+        // ---- write back, a5 usage scatter
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             const int32_t q = q0 + gl + G * t;
-            const bool ok = active && q < q1;
-            if (ok) st256(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k = 4 * t + e;
-                const int j = ok ? idx[k] : (int)S.N;
-                double c = yv[k];
-                if constexpr (SAMPLED) c -= yold[k];
-                if (j >= H && j < S.N) atomicAdd(S.s + j, c);
-                stv[k * 32 + lane] = c;
-                sti[k * 32 + lane] = j < H ? j : -1;
-            }
+            if (active && q < q1) st256(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
-        if (active && gl == 0) S.y0[i] = y0new;
-        if (H > 0) {
-            __syncwarp();
-            // one segment of the warp at a time; its G*NE staged updates hit distinct ids
+        if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+        if constexpr (SAMPLED) {
 #pragma unroll
-            for (int gg = 0; gg < GPW; ++gg) {
-#pragma unroll
-                for (int u = lane; u < G * NE; u += 32) {
-                    const int p = (u / G) * 32 + gg * G + (u % G);   // entry u / G of lane gg*G + u % G
-                    const int j = sti[p];
-                    if (j >= 0) hw[j] += stv[p];
-                }
-                __syncwarp();
-            }
+            for (int e = 0; e < NE; ++e) yv[e] -= yold[e];
         }
+        scatter_group<NE>(idx, yv, hg, HH, S.s, N);
     }
     if constexpr (!ARGMAX) {
-        if (gl == 0 && passes_acc) {
-            atomicAdd(S.counters + 1, passes_acc);
-            if (fail_acc) atomicAdd(S.counters + 0, fail_acc);
-            if (restart_acc) atomicAdd(S.counters + 2, restart_acc);
+        if (st.passes) {
+            atomicAdd(S.counters + 1, st.passes);
+            if (st.failures) atomicAdd(S.counters + 0, st.failures);
+            if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
         }
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < H; j += kPrimalThreads) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) sum += sm.hist[w][j];
-        if (sum != 0.0) atomicAdd(S.s + j, sum);
-    }
+    flush_hists(sm.hist, WARPS * GPW, HS, HH, N, S.s);
 }
 
 }  // namespace spfom
