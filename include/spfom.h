@@ -206,6 +206,15 @@ spfom_status spfom_info(const spfom_handle *h, spfom_info_t *out);
  * summed milliseconds to ms[0] (K1) and ms[1] (rest).  Advances the iterate. */
 spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms);
 
+/* Timed stepping (bench.py's timed region): enqueue k iterations exactly like
+ * spfom_step -- each iteration replays two CUDA graphs, the primal kernels
+ * (a1-a5) and the rest (a6-a8 + tick), with a CUDA event recorded on the
+ * handle's stream before and after the primal graph -- then synchronise and
+ * write ms[0] = summed event time of the primal kernels over the k iterations,
+ * ms[1] = event time from the first to the last event (all k iterations).
+ * Collective when world > 1.  Advances the iterate by k. */
+spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms);
+
 int64_t spfom_iteration(const spfom_handle *h);
 const char *spfom_last_error(const spfom_handle *h); /* NULL handle => thread's last create error */
 void spfom_destroy(spfom_handle *h);

@@ -62,7 +62,11 @@ thread_local std::string g_create_error;
 
 // Bin = (G lanes per segment, Q quads per lane) -> capacity 4 G Q entries.
 // (G lanes per segment, Q quads per lane); capacities 16 .. 1024 entries.
-#define SPFOM_BINS(X) X(0, 4, 1) X(1, 4, 2) X(2, 8, 2) X(3, 16, 2) X(4, 32, 2) X(5, 32, 4) X(6, 32, 8)
+#ifndef SPFOM_BIN2_G
+#define SPFOM_BIN2_G 4   // 8 segments per warp: the per-warp Newton / reduction overhead is shared by more rows
+#define SPFOM_BIN2_Q 4
+#endif
+#define SPFOM_BINS(X) X(0, 4, 1) X(1, 4, 2) X(2, SPFOM_BIN2_G, SPFOM_BIN2_Q) X(3, 16, 2) X(4, 32, 2) X(5, 32, 4) X(6, 32, 8)
 struct BinCfg { int G, Q; };
 #define SPFOM_BIN_INIT(B, G, Q) {G, Q},
 constexpr BinCfg kBins[] = {SPFOM_BINS(SPFOM_BIN_INIT)};
@@ -162,6 +166,7 @@ struct spfom_handle {
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
+    cudaGraphExec_t graph_primal = nullptr, graph_rest = nullptr, graph_rest_refresh = nullptr;   // split (timed) form
     std::string err;
     int sm_count = 148;
     bool own_stream = false;
@@ -229,15 +234,16 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
     L.hh = (int32_t)std::min<int64_t>(StreamLayout<G, Q>::HH, S.N);
     const int64_t rounds = (L.count + StreamLayout<G, Q>::GPW - 1) / StreamLayout<G, Q>::GPW;
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + kStreamWarps - 1) / kStreamWarps));
-    k_primal_stream<G, Q, ARGMAX><<<(unsigned)blocks, kStreamThreads, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+    constexpr int W = StreamLayout<G, Q>::WARPS;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
+    k_primal_stream<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
 void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q)                                                                      \
     case B:                                                                                \
-        if constexpr (Q <= 2) {                                                            \
+        if constexpr (Q <= 4) {                                                            \
             if (argmax) launch_stream<G, Q, true>(S, L, sms, st);                          \
             else launch_stream<G, Q, false>(S, L, sms, st);                                \
         }                                                                                  \
@@ -294,7 +300,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             // full sweep: the bin is the contiguous device range [bin_first[b], bin_first[b+1])
             const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];
             if (cnt == 0) continue;
-            if (kBins[b].Q <= 2) {
+            if (kBins[b].Q <= 4) {
                 StreamList SL{};
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
@@ -353,10 +359,12 @@ spfom_status enqueue_iteration(spfom_handle *h, bool refresh) {
     return st != SPFOM_OK ? st : enqueue_rest(h, refresh, nullptr);
 }
 
-spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out) {
+// part: 0 = whole iteration, 1 = primal kernels only, 2 = the rest
+spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, int part = 0) {
     cudaGraph_t g;
     CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    spfom_status st = enqueue_iteration(h, refresh);
+    spfom_status st = part == 0 ? enqueue_iteration(h, refresh)
+                    : part == 1 ? enqueue_primal(h, nullptr) : enqueue_rest(h, refresh, nullptr);
     cudaGraph_t gg;
     cudaError_t e = cudaStreamEndCapture(h->stream, &gg);
     if (st != SPFOM_OK) return st;
@@ -693,9 +701,12 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.sampled = pl.sampled ? 1 : 0;
 
     st = build_graph(h, false, &h->graph);
+    if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
+    if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_rest, 2);
     if (st != SPFOM_OK) return bail(st);
     if (pl.sampled && p->refresh_every > 0) {
         st = build_graph(h, true, &h->graph_refresh);
+        if (st == SPFOM_OK) st = build_graph(h, true, &h->graph_rest_refresh, 2);
         if (st != SPFOM_OK) return bail(st);
     }
     *out = h;
@@ -942,6 +953,42 @@ spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms) {
     return SPFOM_OK;
 }
 
+spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
+    if (!h || !ms || k < 1) return SPFOM_EINVAL;
+    std::vector<cudaEvent_t> ev(2 * k + 1);
+    for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
+    spfom_status st = SPFOM_OK;
+    for (int64_t it = 0; it < k && st == SPFOM_OK; ++it) {
+        const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
+        cudaError_t e = cudaEventRecord(ev[2 * it], h->stream);
+        if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_primal, h->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * it + 1], h->stream);
+        if (e == cudaSuccess) e = cudaGraphLaunch(refresh ? h->graph_rest_refresh : h->graph_rest, h->stream);
+        if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
+        h->iter += 1;
+    }
+    if (st == SPFOM_OK && cudaEventRecord(ev[2 * k], h->stream) != cudaSuccess)
+        st = fail(h, SPFOM_ECUDA, "spfom_step_timed: final event");
+    double primal = 0.0, total = 0.0;
+    if (st == SPFOM_OK) {
+        cudaError_t e = cudaEventSynchronize(ev[2 * k]);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        for (int64_t it = 0; it < k && e == cudaSuccess; ++it) {
+            float a = 0.f;
+            e = cudaEventElapsedTime(&a, ev[2 * it], ev[2 * it + 1]);
+            primal += a;
+        }
+        float tt = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&tt, ev[0], ev[2 * k]);
+        total = tt;
+        if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed events: ") + cudaGetErrorString(e));
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    ms[0] = primal;
+    ms[1] = total;
+    return st;
+}
+
 int64_t spfom_iteration(const spfom_handle *h) { return h ? h->iter : -1; }
 
 const char *spfom_last_error(const spfom_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
@@ -951,6 +998,8 @@ void spfom_destroy(spfom_handle *h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->graph_refresh) cudaGraphExecDestroy(h->graph_refresh);
+    for (cudaGraphExec_t g : {h->graph_primal, h->graph_rest, h->graph_rest_refresh})
+        if (g) cudaGraphExecDestroy(g);
     if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;

@@ -16,7 +16,10 @@ constexpr int kPrimalThreads = 128; // K1: 4 warps per block, 4 blocks per SM
 #endif
 constexpr int kPrimalMinBlocks = SPFOM_PRIMAL_MIN_BLOCKS;
 constexpr int kHeadMax = 1024;      // products privatised in shared memory (Zipf head)
-constexpr int kGHeadStreamMax = 4096;   // K1 stream: head of g staged in shared memory
+#ifndef SPFOM_GHEAD_MAX
+#define SPFOM_GHEAD_MAX 4096
+#endif
+constexpr int kGHeadStreamMax = SPFOM_GHEAD_MAX;   // K1 stream: head of g staged in shared memory
 
 struct DevState {
     // per quad (4 padded entries), relabelled product ids, rows sorted by new id

@@ -338,8 +338,19 @@ __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 #ifndef SPFOM_SPREAD_C
 #define SPFOM_SPREAD_C 8
 #endif
+#ifndef SPFOM_HIST_TOTAL
+#define SPFOM_HIST_TOTAL 1024      // head products privatised per warp (split over its groups)
+#endif
+#ifndef SPFOM_STREAM_WARPS
+#define SPFOM_STREAM_WARPS 12        // 8 entries per lane: 168 registers -> 12 warps per SM
+#endif
+#ifndef SPFOM_STREAM_WARPS_WIDE
+#define SPFOM_STREAM_WARPS_WIDE 8    // 16 entries per lane
+#endif
 template <int G, int Q>
 struct StreamLayout {
+    // one persistent block per SM; warps per block from the register budget
+    static constexpr int WARPS = (4 * Q >= 16) ? SPFOM_STREAM_WARPS_WIDE : SPFOM_STREAM_WARPS;
     static constexpr int GPW = 32 / G;                 // segments per round (per warp)
     static constexpr int QMAX = GPW * G * Q;           // quads per round, at most
     static constexpr int QW = ((GPW + 8) + 3) & ~3;    // qoff window of the next round (ints)
@@ -355,13 +366,11 @@ struct StreamLayout {
     static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
     // head products per histogram: one per group (GPW of them) or one per warp
     static constexpr int NHIST = SPFOM_WARP_HIST ? 1 : GPW;
-    static constexpr int HH = 1024 / NHIST;
+    static constexpr int HH = SPFOM_HIST_TOTAL / NHIST;
     static constexpr uint32_t HIST = (uint32_t)NHIST * hist_stride(HH) * 8u;   // bytes per warp
     static constexpr uint32_t PER_WARP = SLOT + ((HIST + 127u) & ~127u);
 };
 
-constexpr int kStreamWarps = 12;            // one persistent block of 12 warps per SM (168 registers)
-constexpr int kStreamThreads = 32 * kStreamWarps;
 
 struct StreamList {
     int64_t first, count;   // segments [first, first + count), all of one bin
@@ -371,11 +380,11 @@ struct StreamList {
 
 template <int G, int Q>
 __host__ __device__ constexpr size_t stream_smem_fixed() {
-    return (size_t)kStreamWarps * StreamLayout<G, Q>::PER_WARP + 128;   // + mbarriers
+    return (size_t)StreamLayout<G, Q>::WARPS * StreamLayout<G, Q>::PER_WARP + 128;   // + mbarriers
 }
 
 template <int G, int Q, bool ARGMAX>
-__global__ void __launch_bounds__(kStreamThreads, 1) k_primal_stream(DevState S, StreamList L) {
+__global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_stream(DevState S, StreamList L) {
     using LY = StreamLayout<G, Q>;
     constexpr int NE = 4 * Q;
     constexpr int GPW = LY::GPW;
@@ -394,15 +403,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_primal_stream(DevState S,
 
     unsigned char *slot = smem + (size_t)warp * LY::PER_WARP;
     double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)kStreamWarps * LY::PER_WARP) + warp;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + warp;
     double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q>());
     double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) +
                  (LY::NHIST > 1 ? gidx * HS : 0);
     const int spread_n = S.spread_n;
-    const int spread_rel = S.spread_off + ((blockIdx.x * kStreamWarps + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
+    const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
     for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
-    for (int w = 0; w < kStreamWarps; ++w) {
+    for (int w = 0; w < LY::WARPS; ++w) {
         double *h = reinterpret_cast<double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
         for (int j = threadIdx.x; j < LY::NHIST * HS; j += blockDim.x) h[j] = 0.0;
     }
@@ -421,8 +430,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_primal_stream(DevState S,
 
     // this warp's rounds [r0, r1) of GPW consecutive segments
     const int64_t rounds = (L.count + GPW - 1) / GPW;
-    const int64_t W = (int64_t)gridDim.x * kStreamWarps;
-    const int64_t gw = (int64_t)blockIdx.x * kStreamWarps + warp;
+    const int64_t W = (int64_t)gridDim.x * LY::WARPS;
+    const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
     const int64_t r0 = rounds * gw / W, r1 = rounds * (gw + 1) / W;
 
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_primal_stream(DevState S,
         const int lim = HH < N ? HH : N;
         for (int j = threadIdx.x; j < lim; j += blockDim.x) {
             double sum = 0.0;
-            for (int w = 0; w < kStreamWarps; ++w) {
+            for (int w = 0; w < LY::WARPS; ++w) {
                 const double *h = reinterpret_cast<const double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
 #pragma unroll
                 for (int g2 = 0; g2 < LY::NHIST; ++g2) sum += h[g2 * HS + j];

@@ -60,6 +60,32 @@ def sass_profile(rep):
     return stalls, mix, sass_tags
 
 
+ITER_KERNELS = ("k_primal", "k_fold", "k_dual", "k_tick", "k_average")   # launched every iteration
+
+
+def write_launch_summary(rnd, path):
+    """Per-kernel launch counts and average gpu__time_duration from an ncu
+    --metrics gpu__time_duration.sum launch list; shares of one iteration."""
+    rows = [r for r in csv.reader(open(path)) if len(r) > 14 and r[12] == "gpu__time_duration.sum"]
+    agg = collections.OrderedDict()
+    for r in rows:
+        name = r[4]
+        agg.setdefault(name, []).append(float(r[14]) / 1e3)      # us
+    it_total = sum(sum(v) / len(v) for k, v in agg.items()
+                   if any(x in k for x in ITER_KERNELS))
+    lines = [f"ncu --metrics gpu__time_duration.sum --clock-control none launch list ({os.path.basename(path)}),",
+             "cold-cache and serialised: compare shares, not absolutes.  Per-iteration kernels: " +
+             ", ".join(ITER_KERNELS) + "; k_usage / k_resid_* run once for the residuals call outside the timed loop.",
+             ""]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
+        avg = sum(v) / len(v)
+        per_iter = any(x in k for x in ITER_KERNELS)
+        share = f"{avg / it_total * 100:5.1f}% of iteration" if per_iter and it_total else "(not in the iteration)"
+        lines.append(f"  {len(v):4d} launches  avg {avg:9.1f} us   {share}  {k}")
+    open(os.path.join(HERE, f"{rnd}_launches_summary.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 def main():
     rnd, rep = sys.argv[1], sys.argv[2]
     launches = sys.argv[3] if len(sys.argv) > 3 else None
@@ -87,6 +113,7 @@ def main():
     json.dump(summ, open(summ_path, "w"), indent=1)
     if launches:
         shutil.copy(launches, os.path.join(HERE, f"{rnd}_launches.csv"))
+        write_launch_summary(rnd, launches)
     print("\n".join(lines))
 
 

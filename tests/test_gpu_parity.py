@@ -168,6 +168,23 @@ def test_checkpoint_resume():
     b.close()
 
 
+def test_step_timed_is_step():
+    """The timed stepping bench.py uses (two graphs per iteration, events around
+    the primal graph) computes the same iterates as spfom_step."""
+    from paper_2602_22421_b200 import Solver
+    inst = generate("medium", m=3000, N=2000, k=(20, 200))
+    a, b = Solver(inst, _params()), Solver(inst, _params())
+    a.step(12)
+    primal_ms, total_ms = b.step_timed(12)
+    assert b.iteration == a.iteration == 12 and 0.0 < primal_ms <= total_ms
+    ya, y0a = a.primal()
+    yb, y0b = b.primal()
+    assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(y0b, y0a, 1.0) <= 1e-12
+    assert rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
 # ------------------------------------------------------------ accuracy gates
 @pytest.mark.parametrize("seed", [1, 11, 12])
 def test_tiny_accuracy_vs_dense_lp(seed):
