@@ -113,6 +113,16 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) 
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
 }
+// shared-memory fp64 access through a 32-bit shared-window address (keeps
+// ptxas from rebuilding the generic->shared conversion in predicated code)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double x;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double x) {
+    asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(x) : "memory");
+}
 // fp64 reduction into global memory under a predicate, without a branch
 __device__ __forceinline__ void red_add_if(double *p, double v, bool pred) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p red.global.add.f64 [%0], %1;\n\t}"

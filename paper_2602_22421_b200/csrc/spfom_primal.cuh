@@ -66,7 +66,14 @@ __device__ __forceinline__ bool newton_dir(const double J[3][3], const double R[
     d[0] = -(c00 * R[0] + c10 * R[1] + c20 * R[2]) * inv;   // J^{-1} = adj(J) / det
     d[1] = -(c01 * R[0] + c11 * R[1] + c21 * R[2]) * inv;
     d[2] = -(c02 * R[0] + c12 * R[1] + c22 * R[2]) * inv;
-    return isfinite(d[0]) && isfinite(d[1]) && isfinite(d[2]);
+    return isfinite(d[0] + d[1] + d[2]);                    // one test: inf / NaN propagate into the sum
+}
+
+// max without the NaN-aware fmax expansion (callers test finiteness themselves)
+__device__ __forceinline__ double dmax_sel(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}" : "=d"(r) : "d"(a), "d"(b));
+    return r;
 }
 
 struct PieceSums {
@@ -162,9 +169,12 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
             double sz = 0.0, svt = 0.0, nk = 0.0;
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
+                // opaque copies: keep this rare path from being hoisted out of the loop
+                double ve = v[e], oe = om[e];
+                asm volatile("" : "+d"(ve), "+d"(oe));
                 sz += z[e];
-                svt += fma(-v[e], om[e], v[e]);
-                nk += v[e] > 0.0 ? 1.0 : 0.0;
+                svt += fma(-ve, oe, ve);
+                nk += ve > 0.0 ? 1.0 : 0.0;
             }
             sz = group_sum<G>(sz);
             svt = group_sum<G>(svt);
@@ -216,7 +226,7 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
                 const double swy = fma(x2, ps.cvw, ps.sfwa);
                 const double r1 = fma(-x2, ps.cvv, ps.rva);
                 const double R[3] = {r1 - vt0 * x1, y0c + swy - vt0 * x2, y0c + sy - lam};
-                const double nr = fmax(fabs(R[0]), fmax(fabs(R[1]), fabs(R[2])));
+                const double nr = dmax_sel(fabs(R[0]), dmax_sel(fabs(R[1]), fabs(R[2])));   // NaN -> caught below
                 bool done = !(nr > tol);
                 if (!isfinite(nr)) { done = true; failed = true; }
                 if (!done) {
@@ -407,6 +417,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
     double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q>());
     double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) +
                  (LY::NHIST > 1 ? gidx * HS : 0);
+    const uint32_t ghead_s = smem_u32(ghead), hg_s = smem_u32(hg);
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
-            const double gj = (j < HG) ? ghead[j] : __ldg(S.g + j);
+            const double gj = (j < HG) ? lds_f64(ghead_s + 8u * (uint32_t)j) : __ldg(S.g + j);
             if constexpr (ARGMAX) z[e] = gj;             // theta = inf: keep g itself
             else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
         }
@@ -547,7 +558,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
                 const int j = idx[e];
-                if (j < HH) hg[j] += yv[e];
+                if (j < HH) {
+                    const uint32_t a = hg_s + 8u * (uint32_t)j;
+                    sts_f64(a, lds_f64(a) + yv[e]);
+                }
             }
         } else {
 #pragma unroll
