@@ -41,6 +41,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-iters", type=int, default=50, help="unused (kept for old command lines)")
     ap.add_argument("--cache", default=None, help="directory to cache the generated instance (npz)")
+    ap.add_argument("--stacked", action="store_true",
+                    help="multi-period configs: pass the stacked instance as one period (no shared structure)")
     return ap.parse_args()
 
 
@@ -207,7 +209,9 @@ def run_reference(args, rank, world):
 
 
 def workload_config(inst, world):
-    return {"workload": inst.name, "m": inst.m, "N": inst.N, "nnz": inst.nnz, "preset": "converge",
+    T = int(inst.meta.get("T", 1))
+    extra = {"periods": T, "layout": "shared structure (num_periods = T)"} if T > 1 else {}
+    return {"workload": inst.name, "m": inst.m, "N": inst.N, "nnz": inst.nnz, **extra, "preset": "converge",
             "theta": 1.0, "tau": "0.9/n_j", "extrapolation": 1.0, "mu": 0.0, "block": "full sweep",
             "parallelism": f"segments sharded over {world} GPU(s) by nnz; NCCL allreduce of s each iteration"
             if world > 1 else "1 GPU",
@@ -238,16 +242,29 @@ def main():
         dist.init_process_group("nccl", device_id=device)
 
     inst = load_instance(args.config, args.cache)
-    bounds = partition(inst.seg_ptr, world)
-    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    shard = inst.segment_slice(lo, hi) if world > 1 else inst
+    T = int(inst.meta.get("T", 1))
+    if T > 1:
+        # multi-period: whole base segments (all T periods) per rank, shared structure
+        from spfom_inputs import period_slice
+        mb = int(inst.meta.get("m_per_period", inst.m // T))
+        bounds = partition(inst.seg_ptr[: mb + 1], world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        shard = period_slice(inst, lo, hi) if world > 1 else inst
+    else:
+        bounds = partition(inst.seg_ptr, world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        shard = inst.segment_slice(lo, hi) if world > 1 else inst
     nid = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     params = Params.converge()
-    kw = dict(device=device, rank=rank, world=world, nccl_id=nid, segment_offset=lo, num_segments_global=inst.m)
+    kw = dict(device=device, rank=rank, world=world, nccl_id=nid, segment_offset=lo,
+              num_segments_global=inst.m if T == 1 else int(inst.meta.get("m_per_period", inst.m // T)),
+              shared_periods=not args.stacked)
+    if args.stacked:
+        T = 1
 
     def barrier():
         if world > 1:
@@ -292,9 +309,12 @@ def main():
     solver.close()
 
     peak, peak_src = measured_peaks()
-    k1_bytes = BYTES_PER_NNZ * shard.nnz + BYTES_PER_SEGMENT * shard.m
+    # algorithmic K1 bytes: structure (ids 4 + v 8 + omega 8) once per base entry, y r/w 16 per
+    # (period) entry; offset 4 per base segment, lambda 8 + vt0 8 + y0 r/w 16 per (period) segment
+    # (T = 1: 36 B/nnz + 36 B/segment)
+    k1_bytes = 20 * shard.nnz // T + 16 * shard.nnz + 4 * shard.m // T + 32 * shard.m
     k1_achieved = k1_bytes / (k1_ms / 1e3) / 1e9
-    iter_bytes = BYTES_PER_NNZ * inst.nnz + BYTES_PER_SEGMENT * inst.m + BYTES_PER_PRODUCT * inst.N
+    iter_bytes = (20 * inst.nnz // T + 16 * inst.nnz + 4 * inst.m // T + 32 * inst.m) + BYTES_PER_PRODUCT * inst.N
     traffic = ncu_traffic()
 
     # e2e through the public API with host buffers: create (H2D) + K steps + duals/primal (D2H)
@@ -335,7 +355,10 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_primal (K1: gather + gradient step + projection + A y scatter)",
                          "achieved": k1_achieved, "peak": peak, "unit": "GB/s", "frac": k1_achieved / peak,
                          "traffic": traffic, "bytes_per_launch": k1_bytes,
-                         "bytes_rule": f"{BYTES_PER_NNZ} B/nnz x {shard.nnz} + {BYTES_PER_SEGMENT} B/segment x {shard.m}",
+                         "bytes_rule": (f"{BYTES_PER_NNZ} B/nnz x {shard.nnz} + {BYTES_PER_SEGMENT} B/segment x {shard.m}"
+                                        if T == 1 else
+                                        f"20 B/base nnz x {shard.nnz // T} + 16 B/nnz x {shard.nnz} + "
+                                        f"4 B/base segment x {shard.m // T} + 32 B/segment x {shard.m} (T = {T} shared)"),
                          "k1_ms_avg": k1_ms, "rest_ms_avg": rest_ms, "k1_share_of_step": k1_ms / (ms / args.steps),
                          "k1_timing": "CUDA events on the solver stream around the primal graph of every timed iteration",
                          "peak_source": peak_src, "frac_of_8tbs": k1_achieved / 8000.0},

@@ -72,6 +72,19 @@ typedef enum {
  *   capacity     [num_products] c_j >= 0 (replicated on every rank)
  *   segment_offset  global id of local segment 0 (sampled blocks use global ids)
  *   num_segments_global  total m over all ranks
+ *   num_periods  T; 0 or 1 = single period.  T > 1: multi-period SBLP with a
+ *                shared structure (reading c15, SPEC stack_periods):
+ *                the CSR arrays, attract, shadow and no_purchase describe the
+ *                num_segments BASE segments once; arrival is [T][num_segments]
+ *                (period-major); segment (t, i) of the stacked SBLP has
+ *                consideration set C_i, weights v_i., w_i., v_i0 and arrival
+ *                arrival[t * num_segments + i], and every period shares one
+ *                inventory c_j.  The device stores the structure once and y as
+ *                [T][entries]; getters return stacked (period-major) order:
+ *                y [T][nnz], y0 [T][num_segments].  n_j (tau_j = tau / n_j)
+ *                counts stacked segments (T x base count).  Sampled blocks are
+ *                not supported with T > 1 (SPFOM_EINVAL); rows must have <= 512
+ *                entries (SPFOM_EDATA).
  * Violations are reported as SPFOM_EDATA.
  */
 typedef struct {
@@ -88,6 +101,7 @@ typedef struct {
     const double *arrival;
     const double *price;
     const double *capacity;
+    int64_t num_periods;
 } spfom_instance;
 
 /*
@@ -197,6 +211,7 @@ typedef struct {
     int64_t bin_segments[8];          /* segments per length bin (G, Q) */
     int32_t bin_G[8], bin_Q[8];
     int32_t num_bins, world;
+    int64_t num_periods;              /* T (1 = single period) */
 } spfom_info_t;
 spfom_status spfom_info(const spfom_handle *h, spfom_info_t *out);
 

@@ -85,7 +85,7 @@ constexpr int kResidBlocks = 592;   // 4 x 148 SMs
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Plan {
-    int64_t m = 0, N = 0, nq = 0;
+    int64_t m = 0, N = 0, nq = 0, T = 1;   // m, nq: base segments / quads; T periods (shared structure)
     int64_t bin_count[kNumBins] = {0};
     int64_t block_entries = 0;      // total local sampled ids
     bool sampled = false;
@@ -110,6 +110,7 @@ int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spre
 void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     pl.m = in->num_segments;
     pl.N = in->num_products;
+    pl.T = std::max<int64_t>(1, in->num_periods);
     pl.nq = 0;
     for (int64_t i = 0; i < pl.m; ++i) {
         int64_t k = in->seg_ptr[i + 1] - in->seg_ptr[i];
@@ -121,15 +122,16 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     pl.sampled = p && p->blocks != nullptr;
     pl.averaging = p && p->averaging;
     pl.block_entries = pl.sampled ? p->block_iters * p->block_size : 0;
-    const int64_t nq = std::max<int64_t>(pl.nq, 1), m = std::max<int64_t>(pl.m, 1), N1 = pl.N + 1;
+    const int64_t nq = std::max<int64_t>(pl.nq, 1), m = std::max<int64_t>(pl.m, 1), N1 = pl.N + 1, T = pl.T;
     size_t sz[O_NSLOTS] = {0};
     sz[O_PIDX] = nq * 16;
-    sz[O_V] = sz[O_OM] = sz[O_Y] = nq * 32;
-    sz[O_YBAR] = pl.averaging ? nq * 32 : 0;
+    sz[O_V] = sz[O_OM] = nq * 32;
+    sz[O_Y] = T * nq * 32;                    // [T][nq] quads
+    sz[O_YBAR] = pl.averaging ? T * nq * 32 : 0;
     sz[O_QOFF] = (m + 1 + 64) * 4;           // + slack: K1's 16-B qoff windows may read past the end
-    sz[O_SEGC] = m * 16;
-    sz[O_SEGV] = m * 32;
-    sz[O_Y0BAR] = pl.averaging ? m * 8 : 0;
+    sz[O_SEGC] = T * m * 16;                  // [T][m]
+    sz[O_SEGV] = T * m * 32;
+    sz[O_Y0BAR] = pl.averaging ? T * m * 8 : 0;
     sz[O_R] = sz[O_C] = sz[O_TAU] = sz[O_ETA] = sz[O_G] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
     sz[O_ACC] = (spread_off(pl.N) + (size_t)kSpreadCopies * spread_range(pl.N)) * 8;   // acc, then spread copies
     sz[O_ETABAR] = pl.averaging ? N1 * 8 : 0;
@@ -159,7 +161,7 @@ struct spfom_handle {
     cudaStream_t stream = nullptr;
     char *ws = nullptr;
     DevState S;
-    int64_t nq = 0, m = 0, N = 0, nnz = 0, n_present = 0;
+    int64_t nq = 0, m = 0, N = 0, nnz = 0, n_present = 0, T = 1;   // base quads / segments / entries; periods
     std::vector<int32_t> new2old, old2new;     // products
     std::vector<int64_t> pos_map;              // original entry -> padded entry
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
@@ -239,6 +241,41 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
     k_primal_stream<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
+// Multi-period shared structure: units = rounds x T over one persistent block per SM.
+template <int G, int Q, bool ARGMAX>
+void launch_mp(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
+    static int hg_cap = -1;
+    constexpr size_t fixed = mp_smem_fixed<G, Q>();
+    if (hg_cap < 0) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
+        cudaFuncSetAttribute(k_primal_mp<G, Q, ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(fixed + (size_t)hg_cap * 8));
+    }
+    L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
+    L.hh = 0;
+    constexpr int W = MPLayout<G, Q>::WARPS;
+    const int64_t units = (L.count + MPLayout<G, Q>::GPW - 1) / MPLayout<G, Q>::GPW * S.T;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (units + W - 1) / W));
+    k_primal_mp<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+}
+
+void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
+    switch (b) {
+#define CASE(B, G, Q)                                                                      \
+    case B:                                                                                \
+        if constexpr (Q <= 4) {                                                            \
+            if (argmax) launch_mp<G, Q, true>(S, L, sms, st);                              \
+            else launch_mp<G, Q, false>(S, L, sms, st);                                    \
+        }                                                                                  \
+        break;
+        SPFOM_BINS(CASE)
+#undef CASE
+    }
+}
+
 void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q)                                                                      \
@@ -271,9 +308,10 @@ void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const 
     }
 }
 
-void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, cudaStream_t st) {
+void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, int64_t seg_off, int64_t quad_off,
+                    cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part); break;
+#define CASE(B, G, Q) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part, seg_off, quad_off); break;
         SPFOM_BINS(CASE)
 #undef CASE
     }
@@ -304,7 +342,8 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 StreamList SL{};
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
-                stream_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
+                if (h->T > 1) mp_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
+                else stream_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
                 ++nl;
                 continue;
             }
@@ -332,7 +371,7 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
         CUDA_TRY(h, cudaMemsetAsync(acc, 0, (h->N + 1) * 8, h->stream));
         if (S.spread_n > 0)
             CUDA_TRY(h, cudaMemsetAsync(S.spread, 0, (size_t)S.spread_c * S.spread_n * 8, h->stream));
-        k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->nq, acc, (int32_t)std::min<int64_t>(kHeadMax, h->N));
+        k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->T * h->nq, acc, (int32_t)std::min<int64_t>(kHeadMax, h->N));
         full_mode = 1;
         ++nl;
     }
@@ -346,7 +385,7 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
     // K3: s_new = full ? acc : s_cur + acc
     k_dual<<<std::max<int64_t>(1, std::min<int64_t>((h->N + kThreads - 1) / kThreads, h->sm_count * 8)), kThreads, 0,
              h->stream>>>(S, full_mode);
-    if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->nq);
+    if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->T * h->nq);
     k_tick<<<1, 1, 0, h->stream>>>(S.t);
     nl += 2 + (h->pl.averaging ? 1 : 0);
     CUDA_TRY(h, cudaGetLastError());
@@ -428,16 +467,24 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
         return fail(nullptr, SPFOM_EINVAL, "instance: missing array or bad size");
     if (in->seg_ptr[0] != 0 || in->seg_ptr[m] != in->nnz)
         return fail(nullptr, SPFOM_EDATA, "instance: seg_ptr[0] must be 0 and seg_ptr[m] == nnz");
+    if (in->num_periods < 0) return fail(nullptr, SPFOM_EINVAL, "instance: num_periods must be >= 0");
+    const int64_t T = std::max<int64_t>(1, in->num_periods);
+    if (T > 1 && p && p->blocks) return fail(nullptr, SPFOM_EINVAL, "sampled blocks are not supported with num_periods > 1");
     if (N >= INT32_MAX) return fail(nullptr, SPFOM_EDATA, "instance: num_products too large");
     for (int64_t i = 0; i < m; ++i) {
         const int64_t a = in->seg_ptr[i], b = in->seg_ptr[i + 1];
         if (b < a) { snprintf(buf, sizeof buf, "seg_ptr not monotone at segment %lld", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
+        if (T > 1 && (b - a + 3) / 4 > 128) {
+            snprintf(buf, sizeof buf, "segment %lld: multi-period rows longer than 512 entries unsupported", (long long)i);
+            return fail(nullptr, SPFOM_EDATA, buf);
+        }
         if ((b - a + 3) / 4 > kMaxQuads) {
             snprintf(buf, sizeof buf, "segment %lld: consideration set of %lld > 1024 products unsupported", (long long)i, (long long)(b - a));
             return fail(nullptr, SPFOM_EDATA, buf);
         }
         if (!(in->no_purchase[i] > 0.0) || !std::isfinite(in->no_purchase[i])) { snprintf(buf, sizeof buf, "no_purchase[%lld] must be > 0", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
-        if (!(in->arrival[i] > 0.0) || !std::isfinite(in->arrival[i])) { snprintf(buf, sizeof buf, "arrival[%lld] must be > 0", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
+        for (int64_t t = 0; t < T; ++t)
+            if (!(in->arrival[t * m + i] > 0.0) || !std::isfinite(in->arrival[t * m + i])) { snprintf(buf, sizeof buf, "arrival[%lld] must be > 0", (long long)(t * m + i)); return fail(nullptr, SPFOM_EDATA, buf); }
         for (int64_t e = a; e < b; ++e) {
             const int32_t j = in->prod_idx[e];
             if (j < 0 || j >= N || (e > a && j <= in->prod_idx[e - 1])) {
@@ -505,6 +552,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     h->N = in->num_products;
     h->nnz = in->nnz;
     h->nq = pl.nq;
+    h->T = pl.T;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -528,7 +576,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
 
     // ---- global column counts n_j
     std::vector<int64_t> counts(N + 1, 0);
-    for (int64_t e = 0; e < in->nnz; ++e) counts[in->prod_idx[e]] += 1;
+    for (int64_t e = 0; e < in->nnz; ++e) counts[in->prod_idx[e]] += h->T;   // stacked segments (T per base row)
     if (h->world > 1) {
         int64_t *dcounts = slot_ptr<int64_t>(h, O_COUNTS);
         if (cudaMemcpyAsync(dcounts, counts.data(), N * 8, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D counts"; return bail(SPFOM_ECUDA); }
@@ -585,8 +633,9 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     const int64_t nq = qoff[m];
     std::vector<int32_t> pidx(4 * std::max<int64_t>(nq, 1), (int32_t)N);
     std::vector<double> vv(4 * std::max<int64_t>(nq, 1), 0.0), om(4 * std::max<int64_t>(nq, 1), 0.0);
-    std::vector<double2> segc(std::max<int64_t>(m, 1));
-    std::vector<double4> segv(std::max<int64_t>(m, 1));
+    const int64_t T = h->T;
+    std::vector<double2> segc(std::max<int64_t>(T * m, 1));
+    std::vector<double4> segv(std::max<int64_t>(T * m, 1));
     h->pos_map.assign(in->nnz, 0);
     bool bad_numeric = false;
 #pragma omp parallel for schedule(dynamic, 4096)
@@ -608,9 +657,12 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             svt += v - w;
             h->pos_map[e] = base + q;
         }
-        segc[k] = make_double2(in->arrival[i], vt0);
-        // y0 = lambda and the initial projection multipliers (nu, kappa, U)
-        segv[k] = make_double4(in->arrival[i], 0.0, 0.0, in->arrival[i] / (vt0 + svt));
+        for (int64_t t = 0; t < T; ++t) {
+            const double lam = in->arrival[t * m + i];
+            segc[t * m + k] = make_double2(lam, vt0);
+            // y0 = lambda and the initial projection multipliers (nu, kappa, U)
+            segv[t * m + k] = make_double4(lam, 0.0, 0.0, lam / (vt0 + svt));
+        }
         if (!std::isfinite(vt0)) bad_numeric = true;
     }
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
@@ -653,17 +705,17 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     auto H2D = [&](int slot, const void *src, size_t bytes) {
         return bytes == 0 || cudaMemcpyAsync(h->ws + h->pl.off[slot], src, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
     };
-    std::vector<double> y0(std::max<int64_t>(m, 1));
-    for (int64_t k = 0; k < m; ++k) y0[k] = segv[k].x;
+    std::vector<double> y0(std::max<int64_t>(T * m, 1));
+    for (int64_t k = 0; k < T * m; ++k) y0[k] = segv[k].x;
     bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
-              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), m * 16) &&
-              H2D(O_SEGV, segv.data(), m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
+              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
+              H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
               H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8);
-    if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), m * 8);
+    if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
-    ok = ok && Z(O_Y, nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
+    ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
          Z(O_COUNTERS, 64) && Z(O_T, 8);
-    if (pl.averaging) ok = ok && Z(O_YBAR, nq * 32) && Z(O_ETABAR, (N + 1) * 8);
+    if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, (N + 1) * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
 
@@ -694,6 +746,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.t = slot_ptr<int64_t>(h, O_T);
     S.m = m;
     S.N = N;
+    S.nq = nq;
+    S.T = (int32_t)T;
     S.theta = p->theta;
     S.mu = p->mu;
     S.omega_x = p->extrapolation;
@@ -755,17 +809,21 @@ spfom_status spfom_usage(spfom_handle *h, double *s) {
 }
 
 // y0 in device order is either a plain array (pitch 8) or the x field of segv (pitch 32)
+// y: device [T][nq] quads -> [T][nnz] stacked entry order
 static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, size_t pitch0, double *y,
                                  double *y0) {
-    std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1)), t0(std::max<int64_t>(h->m, 1));
-    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), dy, h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
+    const int64_t T = h->T;
+    std::vector<double> tmp(4 * std::max<int64_t>(T * h->nq, 1)), t0(std::max<int64_t>(T * h->m, 1));
+    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), dy, T * h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
     if (y0 && h->m)
-        CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, h->m, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, T * h->m, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    if (y)
-        for (int64_t e = 0; e < h->nnz; ++e) y[e] = tmp[h->pos_map[e]];
-    if (y0)
-        for (int64_t k = 0; k < h->m; ++k) y0[h->sorder[k]] = t0[k];
+    for (int64_t t = 0; t < T; ++t) {
+        if (y)
+            for (int64_t e = 0; e < h->nnz; ++e) y[t * h->nnz + e] = tmp[4 * t * h->nq + h->pos_map[e]];
+        if (y0)
+            for (int64_t k = 0; k < h->m; ++k) y0[t * h->m + h->sorder[k]] = t0[t * h->m + k];
+    }
     return SPFOM_OK;
 }
 
@@ -794,7 +852,7 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     DevState S = h->S;
     double *sf = slot_ptr<double>(h, O_TMP);
     CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));
-    k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->nq, sf, (int32_t)std::min<int64_t>(kHeadMax, h->N));
+    k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->T * h->nq, sf, (int32_t)std::min<int64_t>(kHeadMax, h->N));
     spfom_status st = allreduce(h, sf, sf, (size_t)h->N, kNcclFloat64, kNcclSum);
     if (st != SPFOM_OK) return st;
     double *pseg = slot_ptr<double>(h, O_RESSEG);
@@ -806,7 +864,8 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
         L.ids = nullptr;
         L.first = h->bin_first[b];
         L.count = cnt;
-        resid_dispatch(b, S, L, pseg + (size_t)b * kResidBlocks * 4, h->stream);
+        for (int64_t t = 0; t < h->T; ++t)   // partials accumulate over periods (sum / max), see the kernel
+            resid_dispatch(b, S, L, pseg + (size_t)b * kResidBlocks * 4, t * h->m, t * h->nq, h->stream);
     }
     double *pprod = slot_ptr<double>(h, O_RESPROD);
     k_resid_prod<<<kResidBlocks, kThreads, 0, h->stream>>>(S, sf, h->n_present, pprod);
@@ -869,16 +928,19 @@ spfom_status spfom_objective(spfom_handle *h, double *obj) {
 
 spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0, const double *eta, const double *s_prev) {
     if (!h) return SPFOM_EINVAL;
+    const int64_t T = h->T;
     if (y) {
-        std::vector<double> tmp(4 * std::max<int64_t>(h->nq, 1), 0.0);
-        for (int64_t e = 0; e < h->nnz; ++e) tmp[h->pos_map[e]] = y[e];
-        CUDA_TRY(h, cudaMemcpyAsync(h->S.y, tmp.data(), h->nq * 32, cudaMemcpyHostToDevice, h->stream));
+        std::vector<double> tmp(4 * std::max<int64_t>(T * h->nq, 1), 0.0);
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t e = 0; e < h->nnz; ++e) tmp[4 * t * h->nq + h->pos_map[e]] = y[t * h->nnz + e];
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.y, tmp.data(), T * h->nq * 32, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
     if (y0 && h->m) {
-        std::vector<double> t0(h->m);
-        for (int64_t k = 0; k < h->m; ++k) t0[k] = y0[h->sorder[k]];
-        CUDA_TRY(h, cudaMemcpy2DAsync(reinterpret_cast<double *>(h->S.segv), 32, t0.data(), 8, 8, h->m,
+        std::vector<double> t0(T * h->m);
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t k = 0; k < h->m; ++k) t0[t * h->m + k] = y0[t * h->m + h->sorder[k]];
+        CUDA_TRY(h, cudaMemcpy2DAsync(reinterpret_cast<double *>(h->S.segv), 32, t0.data(), 8, 8, T * h->m,
                                       cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
@@ -906,6 +968,7 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
     spfom_handle *h = const_cast<spfom_handle *>(h_);
     memset(out, 0, sizeof *out);
     out->num_segments = h->m;
+    out->num_periods = h->T;
     out->num_products = h->N;
     out->nnz = h->nnz;
     out->nnz_padded = 4 * h->nq;

@@ -46,7 +46,9 @@ struct DevState {
     // counters (device)
     unsigned long long *counters;  // [0] newton failures, [1] passes
     int64_t *t;                    // completed iterations
-    int64_t m, N;
+    int64_t m, N;              // local base segments, products
+    int64_t nq;                // base quads; y, ybar are [T][nq] quads, segc / segv / y0bar [T][m]
+    int32_t T;                 // periods sharing the structure (1 = single period)
     double theta, mu, omega_x;
     int32_t max_newton;
     int32_t sampled;               // 1 => scatter y_new - y_old into s (stale rows kept)
@@ -118,6 +120,12 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
 __device__ __forceinline__ double lds_f64(uint32_t a) {
     double x;
     asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+// ordered variant for data this warp also writes (read-modify-write)
+__device__ __forceinline__ double lds_f64_v(uint32_t a) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
     return x;
 }
 __device__ __forceinline__ void sts_f64(uint32_t a, double x) {

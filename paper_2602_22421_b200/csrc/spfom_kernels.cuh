@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) k_average(DevState S, int64_t nq) {
         ld256(S.ybar + 4 * q, ea, eb, ec, ed);
         st256(S.ybar + 4 * q, ea + (a - ea) * inv, eb + (b - eb) * inv, ec + (c - ec) * inv, ed + (d - ed) * inv);
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S.m; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S.m * S.T; i += (int64_t)gridDim.x * blockDim.x)
         S.y0bar[i] += (S.segv[i].x - S.y0bar[i]) * inv;
 }
 
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_usage(DevState S, int64_t nq, doub
     for (int j = threadIdx.x; j < H; j += blockDim.x) hh[j] = 0.0;
     __syncthreads();
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        const int4 id = S.pidx[q];
+        const int4 id = S.pidx[q < S.nq ? q : q % S.nq];      // y is [T][nq]: the structure repeats
         double y[4];
         ld256(S.y + 4 * q, y[0], y[1], y[2], y[3]);
 #pragma unroll
@@ -94,8 +94,10 @@ __global__ void __launch_bounds__(kThreads) k_usage(DevState S, int64_t nq, doub
 // Per segment: lambda_i z_i*(r - eta) (Dinkelbach on g = r - eta, the price
 // vector k_dual maintains) and the balance / scale / negativity audits of the
 // current iterate; per-block partials [4] = (sum D_seg, max bal, max scale, max neg).
+// Multi-period: launched once per period t with (seg_off, quad_off) = (t m, t nq).
 template <int G, int Q>
-__global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, double *partials) {
+__global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, double *partials, int64_t seg_off,
+                                                        int64_t quad_off) {
     constexpr int NE = 4 * Q;
     __shared__ double red[kThreads / 32][4];
     const int lane = threadIdx.x & 31;
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, d
         double lam = 1.0, vt0 = 1.0, y0 = 1.0;
         int32_t q0 = 0, q1 = 0;
         if (active) {
-            lam = S.segc[i].x; vt0 = S.segc[i].y; y0 = S.segv[i].x; q0 = S.qoff[i]; q1 = S.qoff[i + 1];
+            lam = S.segc[seg_off + i].x; vt0 = S.segc[seg_off + i].y; y0 = S.segv[seg_off + i].x;
+            q0 = S.qoff[i]; q1 = S.qoff[i + 1];
         }
         double v[NE], om[NE], y[NE], gj[NE];
 #pragma unroll
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, d
                 const int64_t p = 4 * (int64_t)q + e;
                 v[4 * t + e] = ok ? S.v[p] : 0.0;
                 om[4 * t + e] = ok ? S.om[p] : 0.0;
-                y[4 * t + e] = ok ? S.y[p] : 0.0;
+                y[4 * t + e] = ok ? S.y[4 * quad_off + p] : 0.0;
                 gj[4 * t + e] = ok ? S.g[idx_of(S.pidx[q], e)] : 0.0;
             }
         }
@@ -182,10 +185,11 @@ __global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, d
         for (int k = 0; k < kThreads / 32; ++k) {
             a += red[k][0]; b = fmax(b, red[k][1]); c = fmax(c, red[k][2]); d = fmax(d, red[k][3]);
         }
-        partials[4 * blockIdx.x + 0] = a;
-        partials[4 * blockIdx.x + 1] = b;
-        partials[4 * blockIdx.x + 2] = c;
-        partials[4 * blockIdx.x + 3] = d;
+        // accumulate: one launch per period writes into the same (zeroed) partials
+        partials[4 * blockIdx.x + 0] += a;
+        partials[4 * blockIdx.x + 1] = fmax(partials[4 * blockIdx.x + 1], b);
+        partials[4 * blockIdx.x + 2] = fmax(partials[4 * blockIdx.x + 2], c);
+        partials[4 * blockIdx.x + 3] = fmax(partials[4 * blockIdx.x + 3], d);
     }
 }
 

@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
                 const int j = idx[e];
                 if (j < HH) {
                     const uint32_t a = hg_s + 8u * (uint32_t)j;
-                    sts_f64(a, lds_f64(a) + yv[e]);
+                    sts_f64(a, lds_f64_v(a) + yv[e]);
                 }
             }
         } else {
@@ -603,6 +603,253 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
                 for (int g2 = 0; g2 < LY::NHIST; ++g2) sum += h[g2 * HS + j];
             }
             if (sum != 0.0) atomicAdd(S.s + j, sum);
+        }
+    }
+}
+
+// ============================================================== k_primal_mp
+// Multi-period shared structure (reading c15; SURVEY §8(a) layout contract):
+// segment (t, i) shares C_i, v_i. and omega_i. with every period; only
+// lambda_{i,t}, y_{.,t}, y0 and the warm start are per period.  The work unit
+// is (round r, period t); units in round-major order are split evenly over the
+// warps.  A warp loads a round's structure (ids, v, omega) once, stages
+// theta g once, then projects each of its periods of that round; the per-entry
+// usage sum_t y_ijt accumulates in shared memory and is scattered once per
+// round, so the structure bytes, the gather and the scatter are T times rarer
+// than in the stacked layout.  Two TMA slots per warp: the structure of round
+// r + 1 and the per-period data of the next unit are fetched while the current
+// unit computes.
+template <int G, int Q>
+struct MPLayout {
+    static constexpr int WARPS = (4 * Q >= 16) ? SPFOM_STREAM_WARPS_WIDE : SPFOM_STREAM_WARPS;
+    static constexpr int GPW = 32 / G;
+    static constexpr int NE = 4 * Q;
+    static constexpr int QMAX = GPW * G * Q;
+    static constexpr int QW = ((GPW + 8) + 3) & ~3;
+    // structure slot (index QMAX of each quad array: inert zero quad)
+    static constexpr uint32_t S_QW = 0;
+    static constexpr uint32_t S_V = ((4u * QW) + 63u) & ~63u;
+    static constexpr uint32_t S_OM = S_V + 32u * (QMAX + 1);
+    static constexpr uint32_t S_IDS = S_OM + 32u * (QMAX + 1);
+    static constexpr uint32_t S_END = ((S_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
+    // period slot
+    static constexpr uint32_t P_SEGV = S_END;                              // double4 x GPW
+    static constexpr uint32_t P_SEGC = P_SEGV + 32u * GPW;                 // double2 x GPW
+    static constexpr uint32_t P_Y = ((P_SEGC + 16u * GPW) + 63u) & ~63u;   // double4 x (QMAX + 1)
+    static constexpr uint32_t P_END = ((P_Y + 32u * (QMAX + 1)) + 127u) & ~127u;
+    // per-lane theta g and usage accumulators, [NE][32 lanes] doubles
+    static constexpr uint32_t GT = P_END;
+    static constexpr uint32_t YS = GT + 256u * NE;
+    static constexpr uint32_t PER_WARP = YS + 256u * NE;
+};
+
+template <int G, int Q>
+__host__ __device__ constexpr size_t mp_smem_fixed() {
+    return (size_t)MPLayout<G, Q>::WARPS * MPLayout<G, Q>::PER_WARP + 256;   // + 2 mbarriers per warp
+}
+
+template <int G, int Q, bool ARGMAX>
+__global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(DevState S, StreamList L) {
+    using LY = MPLayout<G, Q>;
+    constexpr int NE = LY::NE;
+    constexpr int GPW = LY::GPW;
+    static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const int gidx = lane / G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gidx * G));
+    const int N = (int)S.N;
+    const int HG = L.ghead;
+    const int64_t T = S.T, nqb = S.nq, mb = S.m;
+
+    unsigned char *ws = smem + (size_t)warp * LY::PER_WARP;
+    uint64_t *barS = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + 2 * warp;
+    uint64_t *barP = barS + 1;
+    double *ghead = reinterpret_cast<double *>(smem + mp_smem_fixed<G, Q>());
+    const uint32_t ghead_s = smem_u32(ghead);
+    const uint32_t gt_s = smem_u32(ws + LY::GT) + 8u * lane, ys_s = smem_u32(ws + LY::YS) + 8u * lane;
+    const int spread_n = S.spread_n;
+    const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
+
+    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
+    if (lane < 4) {   // inert zero quads
+        reinterpret_cast<double *>(ws + LY::S_V + 32u * LY::QMAX)[lane] = 0.0;
+        reinterpret_cast<double *>(ws + LY::S_OM + 32u * LY::QMAX)[lane] = 0.0;
+        reinterpret_cast<int *>(ws + LY::S_IDS + 16u * LY::QMAX)[lane] = N;
+        reinterpret_cast<double *>(ws + LY::P_Y + 32u * LY::QMAX)[lane] = 0.0;
+    }
+    if (lane == 0) {
+        mbar_init(barS, 1);
+        mbar_init(barP, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int64_t rounds = (L.count + GPW - 1) / GPW;
+    const int64_t units = rounds * T;
+    const int64_t W = (int64_t)gridDim.x * LY::WARPS;
+    const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
+    const int64_t u0 = units * gw / W, u1 = units * (gw + 1) / W;
+
+    auto qload = [&](int64_t r) -> int32_t {
+        int64_t k = GPW * r + (lane < GPW ? lane : GPW);
+        k = k < L.count ? k : L.count;
+        return S.qoff[L.first + k];
+    };
+    // structure of round r (+ the qoff window of round r + 1)
+    auto issueS = [&](int64_t r, int32_t q, bool window) {
+        const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
+        const int64_t s0 = L.first + GPW * r;
+        const uint32_t nq = (uint32_t)(qb - qa);
+        const int64_t w0 = (s0 + GPW) & ~(int64_t)3;
+        const uint32_t wbytes = window ? 4u * LY::QW : 0u;
+        if (lane == 0) {
+            mbar_arrive_expect_tx(barS, 80u * nq + wbytes);
+            if (wbytes) bulk_g2s(ws + LY::S_QW, S.qoff + w0, wbytes, barS);
+            if (nq > 0) {
+                bulk_g2s(ws + LY::S_IDS, S.pidx + qa, 16u * nq, barS);
+                bulk_g2s(ws + LY::S_V, S.v + 4 * (int64_t)qa, 32u * nq, barS);
+                bulk_g2s(ws + LY::S_OM, S.om + 4 * (int64_t)qa, 32u * nq, barS);
+            }
+        }
+    };
+    // period t of round r: segment state and y_t
+    auto issueP = [&](int64_t r, int64_t t, int32_t q) {
+        const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
+        const int64_t s0 = L.first + GPW * r;
+        const int64_t left = L.count - GPW * r;
+        const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
+        const uint32_t nq = (uint32_t)(qb - qa);
+        if (lane == 0) {
+            mbar_arrive_expect_tx(barP, 48u * n + 32u * nq);
+            bulk_g2s(ws + LY::P_SEGV, S.segv + t * mb + s0, 32u * n, barP);
+            bulk_g2s(ws + LY::P_SEGC, S.segc + t * mb + s0, 16u * n, barP);
+            if (nq > 0) bulk_g2s(ws + LY::P_Y, S.y + 4 * (t * nqb + qa), 32u * nq, barP);
+        }
+    };
+
+    ProjStats st;
+    int32_t qc = 0, qn = 0;
+    if (u0 < u1) {
+        const int64_t r = u0 / T;
+        qc = qload(r);
+        issueS(r, qc, (r + 1) * T < u1);
+        issueP(r, u0 % T, qc);
+    }
+    uint32_t phS = 0, phP = 0;
+    int64_t rprev = -1;
+    int idx[NE];
+    double v[NE], om[NE];
+    int32_t qa = 0, qb = 0, base = 0;
+    for (int64_t u = u0; u < u1; ++u) {
+        const int64_t r = u / T, t = u - r * T;
+        if (r != rprev) {
+            // ---- new round: structure into registers, theta g into shared memory
+            mbar_wait(barS, phS);
+            phS ^= 1u;
+            if ((r + 1) * T < u1) {
+                const int64_t s1 = L.first + GPW * (r + 1);
+                int64_t k = GPW * (r + 1) + (lane < GPW ? lane : GPW);
+                k = k < L.count ? k : L.count;
+                qn = reinterpret_cast<const int32_t *>(ws + LY::S_QW)[L.first + k - (s1 & ~(int64_t)3)];
+            }
+            base = __shfl_sync(0xffffffffu, qc, 0);
+            qa = __shfl_sync(0xffffffffu, qc, gidx);
+            qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
+#pragma unroll
+            for (int tq = 0; tq < Q; ++tq) {
+                const int32_t q = qa + gl + G * tq;
+                const int p = q < qb ? q - base : LY::QMAX;
+                const int4 id4 = reinterpret_cast<const int4 *>(ws + LY::S_IDS)[p];
+                idx[4 * tq + 0] = id4.x; idx[4 * tq + 1] = id4.y; idx[4 * tq + 2] = id4.z; idx[4 * tq + 3] = id4.w;
+                const double2 *vp = reinterpret_cast<const double2 *>(ws + LY::S_V) + 2 * p;
+                const double2 *wp = reinterpret_cast<const double2 *>(ws + LY::S_OM) + 2 * p;
+                const double2 v01 = vp[0], v23 = vp[1], w01 = wp[0], w23 = wp[1];
+                v[4 * tq + 0] = v01.x; v[4 * tq + 1] = v01.y; v[4 * tq + 2] = v23.x; v[4 * tq + 3] = v23.y;
+                om[4 * tq + 0] = w01.x; om[4 * tq + 1] = w01.y; om[4 * tq + 2] = w23.x; om[4 * tq + 3] = w23.y;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if ((r + 1) * T < u1) issueS(r + 1, qn, (r + 2) * T < u1);
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int j = idx[e];
+                const double gj = (j < HG) ? lds_f64(ghead_s + 8u * (uint32_t)j) : __ldg(S.g + j);
+                sts_f64(gt_s + 256u * e, ARGMAX ? gj : S.theta * gj);   // a2 (+ the theta of a3)
+                sts_f64(ys_s + 256u * e, 0.0);
+            }
+            rprev = r;
+        }
+        // ---- period t of round r
+        mbar_wait(barP, phP);
+        phP ^= 1u;
+        const int64_t left = L.count - GPW * r;
+        const bool active = gidx < left;
+        const int64_t i = L.first + GPW * r + gidx;      // device base slot
+        double lam = 1.0, vt0 = 1.0;
+        double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
+        if (active) {
+            sv = reinterpret_cast<const double4 *>(ws + LY::P_SEGV)[gidx];
+            const double2 sc = reinterpret_cast<const double2 *>(ws + LY::P_SEGC)[gidx];
+            lam = sc.x;
+            vt0 = sc.y;
+        }
+        double z[NE];
+#pragma unroll
+        for (int tq = 0; tq < Q; ++tq) {
+            const int32_t q = qa + gl + G * tq;
+            const int p = q < qb ? q - base : LY::QMAX;
+            const double2 *yp = reinterpret_cast<const double2 *>(ws + LY::P_Y) + 2 * p;
+            const double2 y01 = yp[0], y23 = yp[1];
+            z[4 * tq + 0] = y01.x; z[4 * tq + 1] = y01.y; z[4 * tq + 2] = y23.x; z[4 * tq + 3] = y23.y;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (u + 1 < u1) {
+            const int64_t rn = (u + 1) / T;
+            issueP(rn, (u + 1) - rn * T, rn == r ? qc : qn);
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const double gt = lds_f64_v(gt_s + 256u * e);
+            z[e] = ARGMAX ? gt : z[e] + gt;                  // a3: z = y + theta g
+        }
+        double yv[NE];
+        double y0new;
+        double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+        if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
+        else project_group<G, NE>(z, v, om, sv.x, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
+
+        // ---- write back y_t and the segment state; accumulate sum_t y
+#pragma unroll
+        for (int tq = 0; tq < Q; ++tq) {
+            const int32_t q = qa + gl + G * tq;
+            if (q < qb)
+                st256(S.y + 4 * (t * nqb + q), yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
+        }
+        if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) sts_f64(ys_s + 256u * e, lds_f64_v(ys_s + 256u * e) + yv[e]);
+
+        // ---- end of this warp's part of round r: a5 scatter of sum_t y
+        if (u + 1 == u1 || (u + 1) / T != r) {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int j = idx[e];
+                const int off = j < spread_n ? spread_rel + j : j;
+                red_add_if(S.s + off, lds_f64_v(ys_s + 256u * e), j < N);
+            }
+            qc = qn;
+        }
+    }
+    if constexpr (!ARGMAX) {
+        if (st.passes) {
+            atomicAdd(S.counters + 1, st.passes);
+            if (st.failures) atomicAdd(S.counters + 0, st.failures);
+            if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
         }
     }
 }

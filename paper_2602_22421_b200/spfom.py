@@ -39,7 +39,7 @@ class _Instance(C.Structure):
                 ("segment_offset", C.c_int64), ("num_segments_global", C.c_int64),
                 ("seg_ptr", C.c_void_p), ("prod_idx", C.c_void_p), ("attract", C.c_void_p),
                 ("shadow", C.c_void_p), ("no_purchase", C.c_void_p), ("arrival", C.c_void_p),
-                ("price", C.c_void_p), ("capacity", C.c_void_p)]
+                ("price", C.c_void_p), ("capacity", C.c_void_p), ("num_periods", C.c_int64)]
 
 
 class _Params(C.Structure):
@@ -65,10 +65,31 @@ class _Info(C.Structure):
                                           "launches_per_iteration", "primal_launches_per_iteration",
                                           "workspace_bytes")] + [
         ("bin_segments", C.c_int64 * 8), ("bin_G", C.c_int32 * 8), ("bin_Q", C.c_int32 * 8),
-        ("num_bins", C.c_int32), ("world", C.c_int32)]
+        ("num_bins", C.c_int32), ("world", C.c_int32), ("num_periods", C.c_int64)]
 
 
 _lib = None
+
+
+def _base_of_stacked(inst, T: int) -> dict:
+    """Base rows of a period-major stacked instance (segment t*m + i = base row i
+    in period t; SPEC stack_periods), checked to really share the structure."""
+    M = int(inst.seg_ptr.shape[0] - 1)
+    if M % T:
+        raise SpfomError(2, f"stacked instance has {M} segments, not a multiple of T = {T}")
+    m = M // T
+    nb = int(inst.seg_ptr[m])
+    seg_ptr = np.asarray(inst.seg_ptr[: m + 1], dtype=np.int64)
+    tiled = dict(prod_idx=nb, attract=nb, shadow=nb, no_purchase=m)
+    for name, n in tiled.items():
+        a = np.asarray(getattr(inst, name))
+        if a.shape[0] != n * T or not np.array_equal(a.reshape(T, n), np.broadcast_to(a[:n], (T, n))):
+            raise SpfomError(2, f"multi-period instance: {name} differs across periods (no shared structure)")
+    if not np.array_equal(np.asarray(inst.seg_ptr).reshape(-1)[1:].reshape(T, m) - np.arange(T)[:, None] * nb,
+                          np.broadcast_to(seg_ptr[1:], (T, m))):
+        raise SpfomError(2, "multi-period instance: consideration sets differ across periods")
+    return dict(seg_ptr=seg_ptr, prod_idx=inst.prod_idx[:nb], attract=inst.attract[:nb], shadow=inst.shadow[:nb],
+                no_purchase=inst.no_purchase[:m], arrival=np.asarray(inst.arrival, dtype=np.float64))
 
 
 def load_library() -> C.CDLL:
@@ -171,7 +192,8 @@ class Solver:
 
     def __init__(self, inst, params: Optional[Params] = None, *, device=None, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 segment_offset: int = 0, num_segments_global: Optional[int] = None):
+                 segment_offset: int = 0, num_segments_global: Optional[int] = None,
+                 shared_periods: bool = True):
         import torch  # device memory and streams only
 
         L = load_library()
@@ -179,19 +201,30 @@ class Solver:
             raise SpfomError(4, "no CUDA device: the SPFOM path has no CPU fallback")
         self.params = params or Params()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        arrays = dict(seg_ptr=inst.seg_ptr, prod_idx=inst.prod_idx, attract=inst.attract, shadow=inst.shadow,
+                      no_purchase=inst.no_purchase, arrival=inst.arrival)
+        # a period-major stacked multi-period instance goes to the shared-structure
+        # layout (num_periods = T): base rows once, arrival [T][m]
+        T = int((getattr(inst, "meta", None) or {}).get("T", 1) or 1)
+        self.periods = T if (shared_periods and T > 1) else 1
+        if self.periods > 1:
+            arrays = _base_of_stacked(inst, T)
         self._keep = dict(
-            seg_ptr=np.ascontiguousarray(inst.seg_ptr, dtype=np.int64),
-            prod_idx=np.ascontiguousarray(inst.prod_idx, dtype=np.int32),
-            attract=_f64(inst.attract), shadow=_f64(inst.shadow), no_purchase=_f64(inst.no_purchase),
-            arrival=_f64(inst.arrival), price=_f64(inst.price), capacity=_f64(inst.capacity))
+            seg_ptr=np.ascontiguousarray(arrays["seg_ptr"], dtype=np.int64),
+            prod_idx=np.ascontiguousarray(arrays["prod_idx"], dtype=np.int32),
+            attract=_f64(arrays["attract"]), shadow=_f64(arrays["shadow"]), no_purchase=_f64(arrays["no_purchase"]),
+            arrival=_f64(arrays["arrival"]), price=_f64(inst.price), capacity=_f64(inst.capacity))
         k = self._keep
-        self.m = k["seg_ptr"].shape[0] - 1
+        mb = k["seg_ptr"].shape[0] - 1
+        nb = k["prod_idx"].shape[0]
+        self.m = mb * self.periods            # stacked sizes: the getters' shapes
         self.N = k["price"].shape[0]
-        self.nnz = k["prod_idx"].shape[0]
-        self._inst = _Instance(self.m, self.N, self.nnz, int(segment_offset),
-                               int(num_segments_global if num_segments_global is not None else self.m),
+        self.nnz = nb * self.periods
+        self._inst = _Instance(mb, self.N, nb, int(segment_offset),
+                               int(num_segments_global if num_segments_global is not None else mb),
                                *[k[n].ctypes.data for n in ("seg_ptr", "prod_idx", "attract", "shadow",
-                                                            "no_purchase", "arrival", "price", "capacity")])
+                                                            "no_purchase", "arrival", "price", "capacity")],
+                               self.periods)
         self._params, self._blocks = self.params._c()
         nbytes = C.c_size_t()
         _check(L.spfom_workspace_bytes(C.byref(self._inst), C.byref(self._params), C.byref(nbytes)))

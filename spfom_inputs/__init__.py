@@ -12,5 +12,6 @@ from .generate import (  # noqa: F401
     block_sequence,
     config_spec,
     generate,
+    period_slice,
     stack_periods,
 )

@@ -267,6 +267,22 @@ def stack_periods(base: Instance, lam_tm: np.ndarray, capacity: np.ndarray,
         meta=dict(meta or {}, T=T, m_per_period=m))
 
 
+def period_slice(inst: Instance, lo: int, hi: int) -> Instance:
+    """Base segments [lo, hi) of a period-major stacked multi-period instance,
+    in every period (a rank's shard when whole segments -- all T periods --
+    stay on one rank); still stacked period-major."""
+    T = int(inst.meta.get("T", 1))
+    m = int(inst.meta.get("m_per_period", inst.m // T))
+    rows = [inst.segment_slice(t * m + lo, t * m + hi) for t in range(T)]
+    nb = rows[0].nnz
+    seg_ptr = np.concatenate([[0]] + [r.seg_ptr[1:] + t * nb for t, r in enumerate(rows)]).astype(np.int64)
+    cat = lambda name: np.concatenate([getattr(r, name) for r in rows])
+    return Instance(name=f"{inst.name}[base {lo}:{hi}]", seg_ptr=seg_ptr, prod_idx=cat("prod_idx"),
+                    attract=cat("attract"), shadow=cat("shadow"), no_purchase=cat("no_purchase"),
+                    arrival=cat("arrival"), price=inst.price, capacity=inst.capacity, present=inst.present,
+                    meta=dict(inst.meta, T=T, m_per_period=hi - lo, shard=(lo, hi)))
+
+
 def block_sequence(m: int, B: int, iters: int, seed: int) -> np.ndarray:
     """Pre-generated sampled blocks I_t ("Randomly generate a subset of
     customers ... with size B"; reading c2): int32 [iters][B], each row B

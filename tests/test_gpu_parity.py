@@ -229,7 +229,30 @@ def _check_sampled_segments(inst, gpu, eta_prev, y_prev, y0_prev, n_sample=3000,
     return worst, y, y0
 
 
-@pytest.mark.parametrize("name", ["medium", "huge"])
+def test_multi_period_shared_structure_equals_stacked():
+    """The shared-structure layout (num_periods = T, K1 k_primal_mp) and the
+    same instance passed stacked as one period (K1 k_primal_stream) compute the
+    same iterates; lengths cross the (4,4), (16,2) and (32,2) bins."""
+    from paper_2602_22421_b200 import Solver
+    inst = generate("multi", m=1500, N=900, k=(20, 200), T=4)
+    a = Solver(inst, _params())
+    b = Solver(inst, _params(), shared_periods=False)
+    assert a.info()["num_periods"] == 4 and b.info()["num_periods"] == 1
+    a.step(30)
+    b.step(30)
+    ya, y0a = a.primal()
+    yb, y0b = b.primal()
+    lam = float(inst.arrival.max())
+    assert rel_inf(ya, yb, lam) <= 1e-12 and rel_inf(y0a, y0b, lam) <= 1e-12
+    assert rel_inf(a.duals(), b.duals(), float(inst.price.max())) <= 1e-12
+    ra, rb = a.residuals(), b.residuals()
+    assert abs(ra["primal_obj"] - rb["primal_obj"]) <= 1e-12 * abs(rb["primal_obj"])
+    assert abs(ra["dual_obj"] - rb["dual_obj"]) <= 1e-12 * abs(rb["dual_obj"])
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("name", ["medium", "huge", "multi"])
 def test_full_size_sampled_outputs(name):
     """BASELINE full sizes in the bench launch configuration: sampled segment
     rows vs the oracle's projection, the usage vector vs a fresh sum, and eta
