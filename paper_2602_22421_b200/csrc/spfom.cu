@@ -72,6 +72,11 @@ struct BinCfg { int G, Q; };
 constexpr BinCfg kBins[] = {SPFOM_BINS(SPFOM_BIN_INIT)};
 #undef SPFOM_BIN_INIT
 constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
+// Wide variant of a bin: the same quad capacity on G*Q lanes (<= 32) with one
+// quad per lane -- shorter per-lane dependency chains for latency-bound launches.
+constexpr int wide_g(int G, int Q) { return G * Q <= 32 ? G * Q : 32; }
+constexpr int wide_q(int G, int Q) { return G * Q / wide_g(G, Q); }
+
 constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
 
 int bin_of(int64_t nq) {
@@ -172,6 +177,11 @@ struct spfom_handle {
     std::string err;
     int sm_count = 148;
     bool own_stream = false;
+    // full sweep with several non-empty bins: one side stream per bin, SM share per bin
+    int nbins_active = 0;
+    int bin_sms[kNumBins] = {0};
+    cudaStream_t side[kNumBins] = {nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[kNumBins] = {nullptr};
 };
 
 namespace {
@@ -276,12 +286,23 @@ void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int
     }
 }
 
+// Throughput config unless the bin gives each warp fewer than two rounds.
+template <int G, int Q>
+bool prefer_wide(int64_t count, int sms) {
+    const int64_t rounds = (count + StreamLayout<G, Q>::GPW - 1) / StreamLayout<G, Q>::GPW;
+    return rounds < 2 * (int64_t)sms * StreamLayout<G, Q>::WARPS;
+}
+
 void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q)                                                                      \
     case B:                                                                                \
         if constexpr (Q <= 4) {                                                            \
-            if (argmax) launch_stream<G, Q, true>(S, L, sms, st);                          \
+            constexpr int WG = wide_g(G, Q), WQ = wide_q(G, Q);                            \
+            if (prefer_wide<G, Q>(L.count, sms) && (WG != G)) {                            \
+                if (argmax) launch_stream<WG, WQ, true>(S, L, sms, st);                    \
+                else launch_stream<WG, WQ, false>(S, L, sms, st);                          \
+            } else if (argmax) launch_stream<G, Q, true>(S, L, sms, st);                   \
             else launch_stream<G, Q, false>(S, L, sms, st);                                \
         }                                                                                  \
         break;
@@ -290,19 +311,23 @@ void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L,
     }
 }
 
+// Segment lists (sampled blocks, rows > 512 entries): register-direct loads,
+// latency-bound launches -> the wide mapping (one quad per lane up to 32 lanes).
 void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int sms,
                      cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q)                                                                      \
-    case B:                                                                                \
+    case B: {                                                                              \
+        constexpr int WG = wide_g(G, Q), WQ = wide_q(G, Q);                                \
         if (argmax) {                                                                      \
-            if (sampled) launch_primal<G, Q, true, true>(S, L, cnt, sms, st);              \
-            else launch_primal<G, Q, true, false>(S, L, cnt, sms, st);                     \
+            if (sampled) launch_primal<WG, WQ, true, true>(S, L, cnt, sms, st);            \
+            else launch_primal<WG, WQ, true, false>(S, L, cnt, sms, st);                   \
         } else {                                                                           \
-            if (sampled) launch_primal<G, Q, false, true>(S, L, cnt, sms, st);             \
-            else launch_primal<G, Q, false, false>(S, L, cnt, sms, st);                    \
+            if (sampled) launch_primal<WG, WQ, false, true>(S, L, cnt, sms, st);           \
+            else launch_primal<WG, WQ, false, false>(S, L, cnt, sms, st);                  \
         }                                                                                  \
-        break;
+        break;                                                                             \
+    }
         SPFOM_BINS(CASE)
 #undef CASE
     }
@@ -324,6 +349,12 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
     const bool argmax = std::isinf(h->params.theta);
     DevState S = h->S;
     int64_t nl = 0;
+    const bool fork = !h->pl.sampled && h->nbins_active > 1;
+    if (fork) {
+        CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->stream));
+        for (int b = 0; b < kNumBins; ++b)
+            if (h->side[b]) CUDA_TRY(h, cudaStreamWaitEvent(h->side[b], h->ev_fork, 0));
+    }
     for (int b = 0; b < kNumBins; ++b) {
         SegList L{};
         L.bin = b;
@@ -342,8 +373,12 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 StreamList SL{};
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
-                if (h->T > 1) mp_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
-                else stream_dispatch(b, argmax, S, SL, h->sm_count, h->stream);
+                // several bins: concurrent persistent kernels on disjoint SM shares
+                // (forked streams; inside a graph they become parallel branches)
+                const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
+                cudaStream_t st = h->nbins_active > 1 ? h->side[b] : h->stream;
+                if (h->T > 1) mp_dispatch(b, argmax, S, SL, sms, st);
+                else stream_dispatch(b, argmax, S, SL, sms, st);
                 ++nl;
                 continue;
             }
@@ -355,6 +390,13 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
         if (maxc == 0) continue;
         primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, h->sm_count, h->stream);
         ++nl;
+    }
+    if (fork) {
+        for (int b = 0; b < kNumBins; ++b)
+            if (h->side[b]) {
+                CUDA_TRY(h, cudaEventRecord(h->ev_join[b], h->side[b]));
+                CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_join[b], 0));
+            }
     }
     CUDA_TRY(h, cudaGetLastError());
     if (launches) *launches = nl;
@@ -384,10 +426,10 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
     if (st != SPFOM_OK) return st;
     // K3: s_new = full ? acc : s_cur + acc
     k_dual<<<std::max<int64_t>(1, std::min<int64_t>((h->N + kThreads - 1) / kThreads, h->sm_count * 8)), kThreads, 0,
-             h->stream>>>(S, full_mode);
+             h->stream>>>(S, full_mode, h->pl.averaging ? 0 : 1);
     if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->T * h->nq);
-    k_tick<<<1, 1, 0, h->stream>>>(S.t);
-    nl += 2 + (h->pl.averaging ? 1 : 0);
+    if (h->pl.averaging) k_tick<<<1, 1, 0, h->stream>>>(S.t);   // else k_dual ticks
+    nl += 1 + (h->pl.averaging ? 2 : 0);
     CUDA_TRY(h, cudaGetLastError());
     if (launches) *launches = nl;
     return SPFOM_OK;
@@ -558,6 +600,11 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev);
     auto bail = [&](spfom_status s) {
         g_create_error = h->err;
+        for (int b = 0; b < kNumBins; ++b) {
+            if (h->side[b]) cudaStreamDestroy(h->side[b]);
+            if (h->ev_join[b]) cudaEventDestroy(h->ev_join[b]);
+        }
+        if (h->ev_fork) cudaEventDestroy(h->ev_fork);
         if (h->own_stream) cudaStreamDestroy(h->stream);
         delete h;
         return s;
@@ -754,6 +801,25 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.max_newton = h->params.max_newton;
     S.sampled = pl.sampled ? 1 : 0;
 
+    // full sweep over several bins: SM shares proportional to each bin's padded entries
+    if (!pl.sampled) {
+        int64_t wtot = 0, w[kNumBins] = {0};
+        for (int b = 0; b < kNumBins; ++b) {
+            w[b] = (int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + (h->bin_first[b + 1] - h->bin_first[b]);
+            if (h->bin_first[b + 1] > h->bin_first[b]) h->nbins_active += 1;
+            wtot += w[b];
+        }
+        if (h->nbins_active > 1) {
+            bool okc = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+            for (int b = 0; b < kNumBins && okc; ++b) {
+                if (h->bin_first[b + 1] == h->bin_first[b]) continue;
+                h->bin_sms[b] = (int)std::max<int64_t>(1, (int64_t)((double)h->sm_count * (double)w[b] / (double)std::max<int64_t>(wtot, 1) + 0.5));
+                okc = cudaStreamCreateWithFlags(&h->side[b], cudaStreamNonBlocking) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&h->ev_join[b], cudaEventDisableTiming) == cudaSuccess;
+            }
+            if (!okc) { h->err = "side stream creation failed"; return bail(SPFOM_ECUDA); }
+        }
+    }
     st = build_graph(h, false, &h->graph);
     if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
     if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_rest, 2);
@@ -984,7 +1050,8 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
         np += out->bin_segments[b] > 0;
     }
     out->primal_launches_per_iteration = np;
-    out->launches_per_iteration = np + 2 + (h->pl.averaging ? 1 : 0);
+    // primal launches + K3 (+ k_average + k_tick with averaging) (+ k_fold when world > 1)
+    out->launches_per_iteration = np + 1 + (h->pl.averaging ? 2 : 0) + (h->world > 1 && h->S.spread_n > 0 ? 1 : 0);
     return SPFOM_OK;
 }
 
@@ -1064,6 +1131,11 @@ void spfom_destroy(spfom_handle *h) {
     for (cudaGraphExec_t g : {h->graph_primal, h->graph_rest, h->graph_rest_refresh})
         if (g) cudaGraphExecDestroy(g);
     if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+    for (int b = 0; b < kNumBins; ++b) {
+        if (h->side[b]) cudaStreamDestroy(h->side[b]);
+        if (h->ev_join[b]) cudaEventDestroy(h->ev_join[b]);
+    }
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
 }

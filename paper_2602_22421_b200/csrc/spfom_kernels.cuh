@@ -18,8 +18,10 @@ namespace spfom {
 // stale rows kept); st = s_new + omega_x (s_new - s_prev);
 // eta = max(0, (1 - tau mu) eta - tau (c - st)); g = r - eta; s_prev = s_new;
 // acc = 0.  a8 (averaging): etabar += (eta - etabar) / t.
-__global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full) {
-    const int64_t t_next = *S.t + 1;
+// tick != 0 (no averaging): the last block to finish also advances the
+// iteration counter (one launch less per iteration than a separate k_tick).
+__global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int32_t tick) {
+    const int64_t t_next = tick ? 0 : *S.t + 1;     // t is only needed for averaging (tick == 0)
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
         double acc = S.s[j];
         if (S.fold_in_dual && j < S.spread_n) {
@@ -37,6 +39,16 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full) {
         S.s_prev[j] = sn;
         S.s[j] = 0.0;
         if (S.etabar) S.etabar[j] += (e - S.etabar[j]) / (double)t_next;
+    }
+    if (tick) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(S.counters + 3, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+                *S.t += 1;
+                S.counters[3] = 0;
+            }
+        }
     }
 }
 

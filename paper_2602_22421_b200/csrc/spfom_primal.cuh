@@ -865,8 +865,12 @@ struct ListSmem {
     double ghead[kHeadMax];                       // price vector g on the head products
 };
 
+// 16+ entries per lane: trade resident blocks for registers (no spills)
+template <int Q>
+constexpr int list_min_blocks() { return Q >= 4 ? 1 : kPrimalMinBlocks; }
+
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
-__global__ void __launch_bounds__(kPrimalThreads, kPrimalMinBlocks) k_primal(DevState S, SegList L) {
+__global__ void __launch_bounds__(kPrimalThreads, list_min_blocks<Q>()) k_primal(DevState S, SegList L) {
     using SM = ListSmem<Q, G>;
     constexpr int NE = 4 * Q;               // entries per lane
     constexpr int GPW = 32 / G;             // segments per warp
