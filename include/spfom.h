@@ -121,6 +121,14 @@ typedef struct {
  *                  t uses row t mod block_iters.  Copied at create.
  *   refresh_every  sampled mode: recompute s = A y from scratch every K
  *                  iterations (0 = never)
+ *   exec_mode      0 = auto; 1 = one CUDA-graph replay per iteration (primal
+ *                  kernels, K3); 2 = persistent cooperative kernel running
+ *                  whole iterations per launch (grid-wide barriers between the
+ *                  primal and dual phases) -- the small regime: world == 1,
+ *                  T == 1, no averaging / refresh, rows <= 1024 entries and at
+ *                  most 4096 segments per iteration (SPFOM_EINVAL otherwise).
+ *                  Auto picks 2 when eligible.  Results are identical up to
+ *                  summation order.
  *   max_newton     cap on projection passes per segment (0 => 200); a segment
  *                  still unconverged after half of it restarts from the cold
  *                  point; one that exhausts it is counted as a failure and
@@ -134,7 +142,7 @@ typedef struct {
     int32_t tau_mode;
     int32_t averaging;
     int32_t max_newton;
-    int32_t reserved0;
+    int32_t exec_mode;
     int64_t block_size;
     int64_t block_iters;
     const int32_t *blocks;

@@ -182,6 +182,9 @@ struct spfom_handle {
     int bin_sms[kNumBins] = {0};
     cudaStream_t side[kNumBins] = {nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join[kNumBins] = {nullptr};
+    // small regime: persistent cooperative kernel, whole iterations per launch
+    bool small = false;
+    int small_q = 1, small_blocks = 0;
 };
 
 namespace {
@@ -801,6 +804,40 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.max_newton = h->params.max_newton;
     S.sampled = pl.sampled ? 1 : 0;
 
+    // small regime (exec_mode 0 auto / 2 forced): whole iterations per cooperative launch
+    {
+        int64_t max_rq = 0;
+        for (int64_t k = 0; k < m; ++k) max_rq = std::max<int64_t>(max_rq, qoff[k + 1] - qoff[k]);
+        const int64_t per_iter = pl.sampled ? p->block_size : m;
+        const bool eligible = h->world == 1 && T == 1 && !pl.averaging && !(pl.sampled && p->refresh_every > 0) &&
+                              max_rq <= 256 && per_iter <= 4096;
+        if (p->exec_mode == 2 && !eligible) {
+            h->err = "exec_mode 2 needs world == 1, T == 1, no averaging/refresh, rows <= 1024 entries, <= 4096 segments per iteration";
+            return bail(SPFOM_EINVAL);
+        }
+        if (eligible && p->exec_mode != 1) {
+            h->small_q = max_rq <= 32 ? 1 : max_rq <= 64 ? 2 : max_rq <= 128 ? 4 : 8;
+            int per_sm = 0;
+            cudaError_t e = cudaSuccess;
+            switch (h->small_q) {
+#define OCC(Q) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<Q, false, false>, kSmallThreads, 0); break;
+                case 1: OCC(1)
+                case 2: OCC(2)
+                case 4: OCC(4)
+                default: OCC(8)
+#undef OCC
+            }
+            int coop = 0;
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+            if (e == cudaSuccess && per_sm >= 1 && coop) {
+                h->small = true;
+                h->small_blocks = h->sm_count;
+            } else if (p->exec_mode == 2) {
+                h->err = "exec_mode 2: cooperative launch unavailable";
+                return bail(SPFOM_EINVAL);
+            }
+        }
+    }
     // full sweep over several bins: SM shares proportional to each bin's padded entries
     if (!pl.sampled) {
         int64_t wtot = 0, w[kNumBins] = {0};
@@ -833,8 +870,54 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     return SPFOM_OK;
 }
 
+}  // extern "C"
+
+template <int Q, bool ARGMAX, bool SAMPLED>
+static cudaError_t launch_small(spfom_handle *h, SmallArgs A) {
+    void *args[] = {(void *)&h->S, (void *)&A};
+    return cudaLaunchCooperativeKernel((const void *)k_small<Q, ARGMAX, SAMPLED>, dim3(h->small_blocks),
+                                       dim3(kSmallThreads), args, 0, h->stream);
+}
+
+template <int Q>
+static cudaError_t small_dispatch_q(spfom_handle *h, const SmallArgs &A) {
+    const bool argmax = std::isinf(h->params.theta);
+    if (h->pl.sampled) return argmax ? launch_small<Q, true, true>(h, A) : launch_small<Q, false, true>(h, A);
+    return argmax ? launch_small<Q, true, false>(h, A) : launch_small<Q, false, false>(h, A);
+}
+
+static spfom_status step_small(spfom_handle *h, int64_t k) {
+    constexpr int64_t kChunk = 1024;                 // iterations per cooperative launch
+    while (k > 0) {
+        SmallArgs A{};
+        if (h->pl.sampled) {
+            A.ids = slot_ptr<int32_t>(h, O_BLKIDS);
+            A.row_off = slot_ptr<int32_t>(h, O_ROWOFF);
+            A.block_iters = h->params.block_iters;
+        }
+        A.nbins = kNumBins;
+        A.full_mode = h->pl.sampled ? 0 : 1;
+        A.t0 = h->iter;
+        A.iters = std::min(k, kChunk);
+        cudaError_t e = cudaSuccess;
+        switch (h->small_q) {
+            case 1: e = small_dispatch_q<1>(h, A); break;
+            case 2: e = small_dispatch_q<2>(h, A); break;
+            case 4: e = small_dispatch_q<4>(h, A); break;
+            default: e = small_dispatch_q<8>(h, A); break;
+        }
+        if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("k_small launch: ") + cudaGetErrorString(e));
+        h->iter += A.iters;
+        k -= A.iters;
+    }
+    return SPFOM_OK;
+}
+
+extern "C" {
+
 spfom_status spfom_step(spfom_handle *h, int64_t k) {
     if (!h || k < 0) return SPFOM_EINVAL;
+    if (h->small) return step_small(h, k);
     for (int64_t it = 0; it < k; ++it) {
         const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
         CUDA_TRY(h, cudaGraphLaunch(refresh ? h->graph_refresh : h->graph, h->stream));

@@ -10,6 +10,9 @@
 #include "spfom_common.cuh"
 #include "spfom_primal.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace spfom {
 
 // ----------------------------------------------------------------- K3
@@ -20,26 +23,30 @@ namespace spfom {
 // acc = 0.  a8 (averaging): etabar += (eta - etabar) / t.
 // tick != 0 (no averaging): the last block to finish also advances the
 // iteration counter (one launch less per iteration than a separate k_tick).
+// a7 for one product j (Eq. 17 with extrapolation and per-product tau_j)
+__device__ __forceinline__ void dual_update(const DevState &S, int64_t j, int32_t full, int64_t t_next) {
+    double acc = S.s[j];
+    if (S.fold_in_dual && j < S.spread_n) {
+        for (int c = 0; c < S.spread_c; ++c) {   // fixed order: deterministic fold of K1's spread copies
+            acc += S.spread[(size_t)c * S.spread_n + j];
+            S.spread[(size_t)c * S.spread_n + j] = 0.0;
+        }
+    }
+    const double sn = full ? acc : S.s_prev[j] + acc;
+    const double sx = fma(S.omega_x, sn - S.s_prev[j], sn);
+    const double tj = S.tau[j];
+    const double e = fmax(0.0, fma(-tj, S.c[j] - sx, (1.0 - tj * S.mu) * S.eta[j]));
+    S.eta[j] = e;
+    S.g[j] = S.r[j] - e;
+    S.s_prev[j] = sn;
+    S.s[j] = 0.0;
+    if (S.etabar) S.etabar[j] += (e - S.etabar[j]) / (double)t_next;
+}
+
 __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int32_t tick) {
     const int64_t t_next = tick ? 0 : *S.t + 1;     // t is only needed for averaging (tick == 0)
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
-        double acc = S.s[j];
-        if (S.fold_in_dual && j < S.spread_n) {
-            for (int c = 0; c < S.spread_c; ++c) {   // fixed order: deterministic fold of K1's spread copies
-                acc += S.spread[(size_t)c * S.spread_n + j];
-                S.spread[(size_t)c * S.spread_n + j] = 0.0;
-            }
-        }
-        const double sn = full ? acc : S.s_prev[j] + acc;
-        const double sx = fma(S.omega_x, sn - S.s_prev[j], sn);
-        const double tj = S.tau[j];
-        const double e = fmax(0.0, fma(-tj, S.c[j] - sx, (1.0 - tj * S.mu) * S.eta[j]));
-        S.eta[j] = e;
-        S.g[j] = S.r[j] - e;
-        S.s_prev[j] = sn;
-        S.s[j] = 0.0;
-        if (S.etabar) S.etabar[j] += (e - S.etabar[j]) / (double)t_next;
-    }
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x)
+        dual_update(S, j, full, t_next);
     if (tick) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -64,6 +71,117 @@ __global__ void __launch_bounds__(kThreads) k_fold(DevState S) {
         S.spread[(size_t)c * S.spread_n + j] = 0.0;
     }
     S.s[j] = acc;
+}
+
+// ----------------------------------------------------------------- small regime
+// Persistent cooperative kernel running `iters` whole iterations in one launch
+// (world == 1, no averaging / refresh): per iteration, a1-a5 over this
+// iteration's segments (one warp per segment, 4 Q entries per lane), grid-wide
+// barrier, a7 over all products, barrier.  Replaces 2 graph nodes + their
+// launch latency per iteration when the per-iteration work is a few thousand
+// segments (small instances, the paper's small sampled blocks).
+struct SmallArgs {
+    const int32_t *ids;        // sampled: block table (device slots), else null (full sweep over [0, m))
+    const int32_t *row_off;    // sampled: [block_iters][nbins + 1]
+    int64_t block_iters;
+    int32_t nbins;
+    int32_t full_mode;         // 1: s = acc (full sweep); 0: s = s_prev + acc (sampled)
+    int64_t t0, iters;         // first iteration index, iterations in this launch
+};
+constexpr int kSmallThreads = 256;
+
+template <int Q, bool ARGMAX, bool SAMPLED>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_small(DevState S, SmallArgs A) {
+    constexpr int G = 32, NE = 4 * Q;
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int N = (int)S.N;
+    const int spread_n = S.spread_n;
+    const int spread_rel = S.spread_off + (int)(gwarp % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
+    ProjStats st;
+    for (int64_t it = 0; it < A.iters; ++it) {
+        const int64_t t = A.t0 + it;
+        const int32_t *ids = nullptr;
+        int64_t cnt = S.m;
+        if constexpr (SAMPLED) {
+            const int32_t *ro = A.row_off + (t % A.block_iters) * (A.nbins + 1);
+            ids = A.ids + ro[0];
+            cnt = ro[A.nbins] - ro[0];
+        }
+        for (int64_t k = gwarp; k < cnt; k += nwarps) {
+            const int64_t i = SAMPLED ? (int64_t)ids[k] : k;
+            const double2 sc = S.segc[i];
+            const double4 sv = S.segv[i];
+            const int32_t q0 = S.qoff[i], q1 = S.qoff[i + 1];
+            int idx[NE];
+            double v[NE], om[NE], z[NE];
+            double yold[SAMPLED ? NE : 1];
+#pragma unroll
+            for (int tq = 0; tq < Q; ++tq) {
+                const int32_t q = q0 + lane + G * tq;
+                double y4[4] = {0.0, 0.0, 0.0, 0.0};
+                if (q < q1) {
+                    const int4 id4 = ld128_nc(S.pidx + q);
+                    idx[4 * tq + 0] = id4.x; idx[4 * tq + 1] = id4.y; idx[4 * tq + 2] = id4.z; idx[4 * tq + 3] = id4.w;
+                    ld256_nc(S.v + 4 * (int64_t)q, v[4 * tq], v[4 * tq + 1], v[4 * tq + 2], v[4 * tq + 3]);
+                    ld256_nc(S.om + 4 * (int64_t)q, om[4 * tq], om[4 * tq + 1], om[4 * tq + 2], om[4 * tq + 3]);
+                    ld256(S.y + 4 * (int64_t)q, y4[0], y4[1], y4[2], y4[3]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        idx[4 * tq + e] = N;
+                        v[4 * tq + e] = 0.0;
+                        om[4 * tq + e] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    z[4 * tq + e] = y4[e];
+                    if constexpr (SAMPLED) yold[4 * tq + e] = y4[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const double gj = S.g[idx[e]];                 // a2 (g[N] = 0 for pads)
+                if constexpr (ARGMAX) z[e] = gj;
+                else z[e] = fma(S.theta, gj, z[e]);            // a3
+            }
+            double yv[NE];
+            double y0new;
+            double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+            if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, sc.x, sc.y, true, yv, y0new);
+            else project_group<G, NE>(z, v, om, sv.x, sc.x, sc.y, true, 0xffffffffu, S.max_newton, x0, x1, x2, yv,
+                                      y0new, st);
+#pragma unroll
+            for (int tq = 0; tq < Q; ++tq) {
+                const int32_t q = q0 + lane + G * tq;
+                if (q < q1) st256(S.y + 4 * (int64_t)q, yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
+            }
+            if (lane == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {                    // a5
+                const int j = idx[e];
+                double c = yv[e];
+                if constexpr (SAMPLED) c -= yold[e];
+                const int off = j < spread_n ? spread_rel + j : j;
+                red_add_if(S.s + off, c, j < N);
+            }
+        }
+        grid.sync();
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x)
+            dual_update(S, j, A.full_mode, 0);                // a7
+        grid.sync();
+    }
+    if constexpr (!ARGMAX) {
+        if (st.passes) {
+            atomicAdd(S.counters + 1, st.passes);
+            if (st.failures) atomicAdd(S.counters + 0, st.failures);
+            if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *S.t += A.iters;
 }
 
 // a8 averaging of the primal (all rows, so that stale rows count in sampled mode)

@@ -45,7 +45,7 @@ class _Instance(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("theta", C.c_double), ("tau", C.c_double), ("mu", C.c_double), ("extrapolation", C.c_double),
                 ("tau_mode", C.c_int32), ("averaging", C.c_int32), ("max_newton", C.c_int32),
-                ("reserved0", C.c_int32), ("block_size", C.c_int64), ("block_iters", C.c_int64),
+                ("exec_mode", C.c_int32), ("block_size", C.c_int64), ("block_iters", C.c_int64),
                 ("blocks", C.c_void_p), ("refresh_every", C.c_int64)]
 
 
@@ -148,6 +148,7 @@ class Params:
     blocks: Optional[np.ndarray] = None      # [iters][B] int32 global ids, rows sorted
     refresh_every: int = 0
     max_newton: int = 200
+    exec_mode: int = 0                        # 0 auto, 1 graph per iteration, 2 persistent small regime
 
     @staticmethod
     def converge(**kw) -> "Params":
@@ -160,7 +161,7 @@ class Params:
     def _c(self):
         blocks = None if self.blocks is None else np.ascontiguousarray(self.blocks, dtype=np.int32)
         p = _Params(float(self.theta), float(self.tau), float(self.mu), float(self.extrapolation), int(self.tau_mode),
-                    int(bool(self.averaging)), int(self.max_newton), 0,
+                    int(bool(self.averaging)), int(self.max_newton), int(self.exec_mode),
                     0 if blocks is None else blocks.shape[1], 0 if blocks is None else blocks.shape[0],
                     None if blocks is None else blocks.ctypes.data, int(self.refresh_every))
         return p, blocks

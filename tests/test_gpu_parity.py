@@ -42,11 +42,35 @@ def _assert_ok(worst):
     ("medium", dict(m=2000, N=1500, k=(20, 200))),          # four length bins, Zipf head
     ("multi", dict(m=400, N=300, k=50, T=3)),               # stacked periods, shared inventory
 ])
-def test_converge_preset_lockstep_100(name, kw):
+@pytest.mark.parametrize("exec_mode", [0, 1])               # auto (persistent small regime here) / graph
+def test_converge_preset_lockstep_100(name, kw, exec_mode):
     inst = generate(name, **kw)
-    worst, gpu, _ = lockstep(inst, _params(), 100)
+    worst, gpu, _ = lockstep(inst, _params(exec_mode=exec_mode), 100)
     gpu.close()
     _assert_ok(worst)
+
+
+@pytest.mark.parametrize("preset,B", [("converge", None), ("converge", 300), ("paper", 40)])
+def test_exec_modes_agree(preset, B):
+    """The persistent cooperative small-regime kernel (exec_mode 2: whole
+    iterations per launch, grid barriers) and the per-iteration graph
+    (exec_mode 1) compute the same iterates."""
+    from paper_2602_22421_b200 import Params, Solver
+    inst = generate("medium", m=1500, N=1200, k=(20, 200))
+    blocks = None if B is None else block_sequence(inst.m, B, 16, 3)
+    mk = (lambda **kw: Params.converge(blocks=blocks, **kw)) if preset == "converge" else \
+         (lambda **kw: Params.paper(blocks=blocks, mu=0.5, **kw))
+    a, b = Solver(inst, mk(exec_mode=2)), Solver(inst, mk(exec_mode=1))
+    a.step(25)
+    b.step(25)
+    assert a.iteration == b.iteration == 25
+    ya, y0a = a.primal()
+    yb, y0b = b.primal()
+    lam = float(inst.arrival.max())
+    assert rel_inf(ya, yb, lam) <= 1e-12 and rel_inf(y0a, y0b, lam) <= 1e-12
+    assert rel_inf(a.duals(), b.duals(), float(inst.price.max())) <= 1e-12
+    a.close()
+    b.close()
 
 
 def _ragged_instance(ks, N=1100, seed=0):
