@@ -5,7 +5,8 @@ reference legs may import this package.  It shares no code with the CUDA path
 (paper_2602_22421_b200/) and never imports it.
 
 * spfom_oracle.c  -- single-threaded fp64 C: projection, exact argmax,
-  FAST-INNER, golden section, one SPFOM iteration, residuals (see its header).
+  FAST-INNER, golden section, one SPFOM iteration, residuals, SBLP->CBLP
+  policy recovery (see its header).
 * lp.py           -- the SBLP / CBLP optimum: textbook dense simplex (Bland)
   and scipy HiGHS (library primitive), plus assortment enumeration.
 
@@ -21,6 +22,8 @@ from .core import (  # noqa: F401
     fast_inner,
     golden,
     lib,
+    policy_probabilities,
     project,
+    recover,
     residual_names,
 )

@@ -76,6 +76,8 @@ def lib():
         L.oracle_primal_shard.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), C.POINTER(_State), _dp]
         L.oracle_dual_apply.restype = None
         L.oracle_dual_apply.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), _dp, _dp, C.POINTER(_State)]
+        L.oracle_recover.restype = None
+        L.oracle_recover.argtypes = [C.c_int64, C.c_double, _dp, _dp, _dp, C.c_double, C.c_double, _ip, _lp, _dp]
         L.oracle_residuals.restype = C.c_int
         L.oracle_residuals.argtypes = [C.POINTER(_Inst), _dp, _dp, _dp, C.c_void_p, _dp]
         _lib = L
@@ -84,6 +86,38 @@ def lib():
 
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def recover(y0, y, v, w, v0, lam, prod):
+    """SBLP -> CBLP recovery of one row (GAM reading): returns
+    (order, alpha) -- row positions of the products by y/v descending (ties:
+    ascending product id) and the probabilities alpha(S_0..S_k) of the nested
+    assortments S_l = first l products (S_0: no-purchase only)."""
+    y, v, w = _f64(y), _f64(v), _f64(w)
+    prod = np.ascontiguousarray(prod, dtype=np.int32)
+    k = y.shape[0]
+    order = np.zeros(k, dtype=np.int64)
+    alpha = np.zeros(k + 1)
+    lib().oracle_recover(k, float(y0), y, v, w, float(v0), float(lam), prod, order, alpha)
+    return order, alpha
+
+
+def policy_probabilities(order, alpha, v, w, v0):
+    """Per-entry sales share of a recovered policy under GAM choice:
+    returns (q0, q) with q_j = sum_l alpha_l pi_j(S_l), q0 = sum_l alpha_l pi_0(S_l),
+    pi_j(S) = v_j / D(S) on S, pi_0(S) = (v0 + sum_{C \\ S} w) / D(S).  Plain
+    definition, used to check the recovery against the row it came from."""
+    v, w = _f64(v), _f64(w)
+    k = v.shape[0]
+    q = np.zeros(k)
+    q0 = 0.0
+    for l in range(k + 1):
+        S = set(int(x) for x in order[:l])
+        D = v0 + sum(v[j] if j in S else w[j] for j in range(k))
+        for j in S:
+            q[j] += alpha[l] * v[j] / D
+        q0 += alpha[l] * (v0 + sum(w[j] for j in range(k) if j not in S)) / D
+    return q0, q
 
 
 def project(z0, z, v, w, v0, lam):

@@ -33,6 +33,10 @@
  *                    (P:L357), extrapolation (reading c8, NOT in the paper),
  *                    dual step Eq. 17 with per-product tau_j,
  *                    optional uniform averaging (reading c9, NOT in the paper).
+ *   oracle_recover   SBLP -> CBLP policy recovery (P:L473-492 Lemma
+ *                    "recover", GAM reading SV App. A.1):
+ *                    nested assortments by y_j / v_j descending and their
+ *                    offer probabilities alpha(S_l).
  *   oracle_residuals objective (Eq. 6), Lagrangian dual bound
  *                    D(eta) = c^T eta + sum_i lambda_i z_i(r - eta),
  *                    infeasibility, certificate (reading c11).
@@ -589,4 +593,55 @@ int oracle_residuals(const oracle_instance *in, const double *eta, const double 
     out[12] = alpha;
     free(s); free(g); free(gb); free(yb);
     return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* SBLP -> CBLP recovery (GAM: SV App. A.1).                    */
+typedef struct { double u; int32_t id; int64_t j; } urank_t;
+
+static int cmp_urank(const void *pa, const void *pb) {
+    const urank_t *a = (const urank_t *)pa, *b = (const urank_t *)pb;
+    if (a->u > b->u) return -1;
+    if (a->u < b->u) return 1;
+    return (a->id < b->id) ? -1 : (a->id > b->id);     /* ties: ascending product index */
+}
+
+/*
+ * One feasible row (y0, y_1..y_k) of segment i with attraction v, shadow
+ * attraction w, no-purchase weight v0 and arrival lambda.  Sort the products
+ * by u_j = y_j / v_j descending (ties by ascending product id prod[j]); the
+ * nested sets S_l are the first l of them (S_0: no product, only the
+ * no-purchase option), l = 0..k.  With vt0 = v0 + sum_j w_j,
+ * U = u_(0) = (y0 + sum_j (w_j / v_j) y_j) / vt0 and u_(k+1) = 0,
+ *     alpha(S_l) = (u_(l) - u_(l+1)) * D(S_l) / lambda,
+ *     D(S) = vt0 + sum_{j in S} (v_j - w_j)
+ * -- the lemma's (y_l / w_l - y_{l+1} / w_{l+1}) * sum_{j in S_l} w_j / lambda
+ * (paper letters: w = attraction, the sum includes option 0) with the GAM
+ * normaliser D(S) = v0 + sum_S v + sum_{C \ S} w.  order[l - 1] receives the
+ * row position j of the l-th product; alpha[0..k] the probabilities.
+ */
+void oracle_recover(int64_t k, double y0, const double *y, const double *v, const double *w, double v0,
+                    double lam, const int32_t *prod, int64_t *order, double *alpha) {
+    urank_t *r = (urank_t *)malloc((size_t)(k > 0 ? k : 1) * sizeof(urank_t));
+    double vt0 = v0, swy = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+        vt0 += w[j];
+        swy += w[j] / v[j] * y[j];
+        r[j].u = y[j] / v[j];
+        r[j].id = prod[j];
+        r[j].j = j;
+    }
+    qsort(r, (size_t)k, sizeof(urank_t), cmp_urank);
+    double D = vt0, prev = (y0 + swy) / vt0;
+    for (int64_t l = 0; l <= k; ++l) {
+        const double next = (l < k) ? r[l].u : 0.0;
+        alpha[l] = (prev - next) * D / lam;
+        if (l < k) {
+            const int64_t j = r[l].j;
+            order[l] = j;
+            D += v[j] - w[j];
+            prev = next;
+        }
+    }
+    free(r);
 }

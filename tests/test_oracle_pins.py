@@ -373,3 +373,66 @@ def test_multi_period_T1_and_stacking():
     b = generate("multi", m=3, N=5, k=3, T=2)
     assert b.m == 2 * a.m and np.array_equal(b.prod_idx[: a.nnz], a.prod_idx)
     assert lp.sblp_dense(b)[0] == pytest.approx(lp.sblp_highs(b)[0], rel=1e-9)
+
+
+# ------------------------------------------------------------ SBLP -> CBLP recovery
+def test_recover_spec_worked_example():
+    """S:L396: m = 1, lambda = 1, w0 = w1 = 1 (MNL), y = (0.75, 0.25) ->
+    alpha({0}) = 0.5, alpha({0,1}) = 0.5 (paper letters: w = attraction)."""
+    order, alpha = oracle.recover(0.75, [0.25], [1.0], [0.0], 1.0, 1.0, [0])
+    assert list(order) == [0] and np.allclose(alpha, [0.5, 0.5], atol=1e-15)
+
+
+def test_recover_degenerate_rows():
+    rng = np.random.default_rng(5)
+    k = 6
+    v = rng.uniform(0.1, 1, k)
+    w = v * rng.uniform(0, 0.5, k)
+    v0, lam = 1.3, 2.0
+    # all mass on the no-purchase option (S:L397): alpha(S_0) = 1
+    _o, a = oracle.recover(lam, np.zeros(k), v, w, v0, lam, np.arange(k))
+    assert abs(a[0] - 1.0) <= 1e-15 and np.all(a[1:] == 0.0)
+    # the full-assortment vertex: every ratio equals U (S:L398) -> one atom on S_k
+    vt0 = v0 + w.sum()
+    U = lam / (vt0 + (v - w).sum())
+    y = v * U
+    y0 = lam - y.sum()
+    _o, a = oracle.recover(y0, y, v, w, v0, lam, np.arange(k))
+    assert abs(a[k] - 1.0) <= 1e-12 and np.all(np.abs(a[:k]) <= 1e-12)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_recover_reproduces_feasible_rows(seed):
+    """The recovered nested-assortment policy reproduces the row it came from
+    under the GAM choice model: lambda sum_l alpha_l pi_j(S_l) = y_j,
+    the same for the no-purchase share, sum alpha = 1, alpha >= 0, and the
+    revenue identity -- checked on rows the oracle projection makes
+    feasible, including capped (tied) entries and zeros."""
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(60):
+        k = int(rng.integers(1, 9))
+        v = rng.uniform(0.1, 1, k)
+        w = v * rng.uniform(0, 0.5, k)
+        v0, lam = rng.uniform(0.5, 2), rng.uniform(1, 10)
+        z = rng.normal(0, 3, k)
+        y0, y, _m, _it = oracle.project(rng.uniform(0, lam), z, v, w, v0, lam)
+        prod = rng.permutation(50)[:k].astype(np.int32)
+        order, alpha = oracle.recover(y0, y, v, w, v0, lam, prod)
+        assert sorted(order) == list(range(k))
+        u = y / v
+        assert all(u[order[i]] >= u[order[i + 1]] for i in range(k - 1))
+        assert abs(alpha.sum() - 1.0) <= 1e-12 and alpha.min() >= -1e-14
+        q0, q = oracle.policy_probabilities(order, alpha, v, w, v0)
+        assert np.abs(lam * q - y).max() <= 1e-12 * lam and abs(lam * q0 - y0) <= 1e-12 * lam
+        r = rng.uniform(1, 10, k)
+        rev = lam * sum(alpha[l] * sum(r[j] * v[j] for j in order[:l]) /
+                        (v0 + sum(v[j] if j in set(order[:l]) else w[j] for j in range(k))) for l in range(k + 1))
+        assert abs(rev - float(r @ y)) <= 1e-11 * max(1.0, float(r @ y))
+
+
+def test_recover_tie_order_by_product_index():
+    """Equal ratios are ordered by ascending product id."""
+    v = np.array([0.5, 0.25, 1.0])
+    y = v * 0.2                      # all ratios equal
+    order, _a = oracle.recover(1.0, y, v, np.zeros(3), 1.0, 1.0 + y.sum(), np.array([7, 3, 5], np.int32))
+    assert list(order) == [1, 2, 0]
