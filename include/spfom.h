@@ -229,6 +229,23 @@ spfom_status spfom_info(const spfom_handle *h, spfom_info_t *out);
  * summed milliseconds to ms[0] (K1) and ms[1] (rest).  Advances the iterate. */
 spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms);
 
+/* SBLP -> CBLP policy recovery of the current iterate (P:L473-492 Lemma
+ * "recover"; GAM reading SV App. A.1), computed on the
+ * device (one warp per segment, in chunks through a workspace scratch area).
+ * For row i (original order; stacked period blocks when num_periods > 1):
+ *   order[seg_ptr[i] .. seg_ptr[i+1])      int32 original product ids sorted by
+ *                                          u_ij = y_ij / v_ij descending, ties by
+ *                                          ascending product id;
+ *   alpha[seg_ptr[i] + i .. seg_ptr[i+1] + i]  probabilities of the nested
+ *                                          assortments S_0 (no product) .. S_k,
+ *                                          S_l = the first l products of order:
+ *   alpha_l = (u_(l) - u_(l+1)) * D(S_l) / lambda_i, u_(0) = U_i =
+ *   (y_i0 + sum_j w_ij / v_ij y_ij) / vt_i0, u_(k+1) = 0,
+ *   D(S) = v_i0 + sum_{j in S} v_ij + sum_{j in C_i \ S} w_ij.
+ * Sizes: order [T][nnz], alpha [T][nnz + num_segments] (caller-owned host
+ * arrays).  Synchronous; SPFOM_ENUMERIC if projection failures were counted. */
+spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha);
+
 /* Timed stepping (bench.py's timed region): enqueue k iterations exactly like
  * spfom_step -- each iteration replays two CUDA graphs, the primal kernels
  * (a1-a5) and the rest (a6-a8 + tick), with a CUDA event recorded on the

@@ -102,7 +102,7 @@ struct Plan {
 enum Slot {
     O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
     O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
-    O_COUNTS, O_NSLOTS
+    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_NSLOTS
 };
 
 constexpr int kSpreadCopies = SPFOM_SPREAD_C;
@@ -111,6 +111,8 @@ constexpr int kSpreadCopies = SPFOM_SPREAD_C;
 #endif
 int64_t spread_range(int64_t N) { return kSpreadCopies > 0 ? std::min<int64_t>(N, SPFOM_SPREAD_N) : 0; }
 int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spread slot after the N + 1 acc slots
+
+int64_t recover_chunk(int64_t nq) { return std::min<int64_t>(std::max<int64_t>(4 * nq, 4096), (int64_t)1 << 22); }
 
 void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     pl.m = in->num_segments;
@@ -148,6 +150,10 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_COUNTERS] = 8 * 8;
     sz[O_T] = 8;
     sz[O_COUNTS] = N1 * 8;
+    // recovery scratch (spfom_recover works in chunks of at most recover_chunk() padded entries)
+    sz[O_RECORD] = (size_t)recover_chunk(pl.nq) * 4;
+    sz[O_RECALPHA] = (size_t)recover_chunk(pl.nq) * 2 * 8;
+    sz[O_ORIG] = N1 * 4;
     size_t o = 0;
     for (int s = 0; s < O_NSLOTS; ++s) {
         pl.off[s] = o;
@@ -170,6 +176,7 @@ struct spfom_handle {
     std::vector<int32_t> new2old, old2new;     // products
     std::vector<int64_t> pos_map;              // original entry -> padded entry
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
+    std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
@@ -687,6 +694,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     std::vector<double2> segc(std::max<int64_t>(T * m, 1));
     std::vector<double4> segv(std::max<int64_t>(T * m, 1));
     h->pos_map.assign(in->nnz, 0);
+    h->seg_off.assign(in->seg_ptr, in->seg_ptr + m + 1);
     bool bad_numeric = false;
 #pragma omp parallel for schedule(dynamic, 4096)
     for (int64_t k = 0; k < m; ++k) {
@@ -760,7 +768,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
               H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
               H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
-              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8);
+              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
+              H2D(O_ORIG, h->new2old.data(), N * 4);
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
     ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
@@ -1200,6 +1209,48 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
     ms[0] = primal;
     ms[1] = total;
     return st;
+}
+
+spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
+    if (!h || !order || !alpha) return SPFOM_EINVAL;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RecoverSmem));
+        attr = true;
+    }
+    const int64_t CH = recover_chunk(h->nq), m = h->m;
+    std::vector<int32_t> qoff(m + 1);
+    CUDA_TRY(h, cudaMemcpyAsync(qoff.data(), h->S.qoff, (m + 1) * 4, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    int32_t *dord = slot_ptr<int32_t>(h, O_RECORD);
+    double *dal = slot_ptr<double>(h, O_RECALPHA);
+    const int32_t *dorig = slot_ptr<int32_t>(h, O_ORIG);
+    std::vector<int32_t> hord(CH);
+    std::vector<double> hal(2 * CH);
+    for (int64_t t = 0; t < h->T; ++t) {
+        for (int64_t a = 0; a < m;) {
+            int64_t b = a + 1;
+            while (b < m && 4 * (int64_t)(qoff[b + 1] - qoff[a]) <= CH && (b + 1 - a) <= CH) ++b;
+            const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(h->sm_count * 2, (b - a + kRecoverWarps - 1) / kRecoverWarps));
+            k_recover<<<(unsigned)blocks, 32 * kRecoverWarps, sizeof(RecoverSmem), h->stream>>>(h->S, a, b, t, dorig, dord, dal);
+            CUDA_TRY(h, cudaGetLastError());
+            const int64_t ne = 4 * (int64_t)(qoff[b] - qoff[a]);
+            if (ne) CUDA_TRY(h, cudaMemcpyAsync(hord.data(), dord, ne * 4, cudaMemcpyDeviceToHost, h->stream));
+            CUDA_TRY(h, cudaMemcpyAsync(hal.data(), dal, (ne + (b - a)) * 8, cudaMemcpyDeviceToHost, h->stream));
+            CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+            for (int64_t k = a; k < b; ++k) {
+                const int64_t i = h->sorder[k];                          // original local segment
+                const int64_t e0 = h->seg_off[i], len = h->seg_off[i + 1] - e0;
+                const int64_t ob = 4 * (int64_t)(qoff[k] - qoff[a]), ab = ob + (k - a);
+                int32_t *o = order + t * h->nnz + e0;
+                double *al = alpha + t * (h->nnz + m) + e0 + i;
+                for (int64_t r = 0; r < len; ++r) o[r] = hord[ob + r];
+                for (int64_t l = 0; l <= len; ++l) al[l] = hal[ab + l];
+            }
+            a = b;
+        }
+    }
+    return check_counters(h);
 }
 
 int64_t spfom_iteration(const spfom_handle *h) { return h ? h->iter : -1; }

@@ -184,6 +184,99 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small(DevState S, SmallArg
     if (blockIdx.x == 0 && threadIdx.x == 0) *S.t += A.iters;
 }
 
+// ----------------------------------------------------------------- recovery
+// SBLP -> CBLP policy recovery (P:L476-492 Lemma "recover", GAM reading
+// SV App. A.1): per segment, the products sorted by u_j = y_j / v_j descending
+// (ties: ascending original product id) and the probabilities of the
+// nested assortments S_l = first l products, l = 0..k:
+//   alpha_l = (u_(l) - u_(l+1)) D(S_l) / lambda,  u_(0) = U, u_(k+1) = 0,
+//   D(S) = vt0 + sum_{j in S} (v_j - w_j).
+// One warp per segment of the device-slot chunk [a, b); rank by counting
+// (k <= 1024), warp-scan of the sorted vt for D.  Outputs for slot k start at
+// 4 (qoff[k] - qoff[a]) (order, original ids) and that + (k - a) (alpha).
+constexpr int kRecoverWarps = 4;
+constexpr int kRecoverMaxK = 1024;
+struct RecoverSmem {
+    double u[kRecoverWarps][kRecoverMaxK];      // row order
+    double vt[kRecoverWarps][kRecoverMaxK];
+    double su[kRecoverWarps][kRecoverMaxK];     // sorted order
+    double svt[kRecoverWarps][kRecoverMaxK];
+    int32_t oid[kRecoverWarps][kRecoverMaxK];
+};
+
+__global__ void __launch_bounds__(32 * kRecoverWarps) k_recover(DevState S, int64_t a, int64_t b, int64_t t,
+                                                                const int32_t *orig_of, int32_t *order_out,
+                                                                double *alpha_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RecoverSmem &sm = *reinterpret_cast<RecoverSmem *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *u = sm.u[warp], *vt = sm.vt[warp], *su = sm.su[warp], *svt = sm.svt[warp];
+    int32_t *oid = sm.oid[warp];
+    const int64_t qa = S.qoff[a];
+    for (int64_t k = a + (int64_t)blockIdx.x * kRecoverWarps + warp; k < b; k += (int64_t)gridDim.x * kRecoverWarps) {
+        const int64_t q0 = S.qoff[k], q1 = S.qoff[k + 1];
+        const double2 sc = S.segc[t * S.m + k];                // (lambda, vt0)
+        const double y0 = S.segv[t * S.m + k].x;
+        const double *yrow = S.y + 4 * (t * S.nq + q0);
+        const int32_t *ids = reinterpret_cast<const int32_t *>(S.pidx + q0);
+        // the row's real entries come first (pads carry id N, the largest relabelled id)
+        const int np = (int)(4 * (q1 - q0));
+        int kk = 0;
+        double swy = 0.0;
+        for (int e = lane; e < np; e += 32) {
+            const int32_t j = ids[e];
+            const bool real = j < S.N;
+            const double v = S.v[4 * q0 + e], om = S.om[4 * q0 + e], y = yrow[e];
+            u[e] = real ? y / v : 0.0;
+            vt[e] = real ? fma(-v, om, v) : 0.0;
+            oid[e] = real ? orig_of[j] : INT32_MAX;
+            swy += real ? om * y : 0.0;
+            kk += real ? 1 : 0;
+        }
+        for (int o = 16; o >= 1; o >>= 1) {
+            swy += __shfl_xor_sync(0xffffffffu, swy, o);
+            kk += __shfl_xor_sync(0xffffffffu, kk, o);
+        }
+        __syncwarp();
+        // rank by counting: u descending, ties by ascending original product id
+        const int64_t ob = 4 * (q0 - qa), ab = ob + (k - a);
+        for (int e = lane; e < kk; e += 32) {
+            const double ue = u[e];
+            const int32_t ie = oid[e];
+            int rank = 0;
+            for (int f = 0; f < kk; ++f) {
+                const double uf = u[f];
+                rank += (uf > ue || (uf == ue && oid[f] < ie)) ? 1 : 0;
+            }
+            su[rank] = ue;
+            svt[rank] = vt[e];
+            order_out[ob + rank] = ie;
+        }
+        __syncwarp();
+        // D_l = vt0 + sum_{r < l} vt_(r): each lane scans one contiguous chunk of l
+        const int per = (kk + 31) / 32;
+        const int l0 = min(kk, lane * per), l1 = min(kk, l0 + per);
+        double part = 0.0;
+        for (int l = l0; l < l1; ++l) part += svt[l];
+        double incl = part;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        double D = sc.y + (incl - part);
+        const double U = (y0 + swy) / sc.y;
+        for (int l = l0; l < l1; ++l) {
+            const double prev = (l == 0) ? U : su[l - 1];
+            alpha_out[ab + l] = (prev - su[l]) * D / sc.x;
+            D += svt[l];
+        }
+        // alpha_k (the full prefix, u_(k+1) = 0): by the lane that ends the last chunk
+        if (kk > 0 && l1 == kk && l0 < l1) alpha_out[ab + kk] = su[kk - 1] * D / sc.x;
+        if (kk == 0 && lane == 0) alpha_out[ab] = U * sc.y / sc.x;
+        __syncwarp();
+    }
+}
+
 // a8 averaging of the primal (all rows, so that stale rows count in sampled mode)
 __global__ void __launch_bounds__(kThreads) k_average(DevState S, int64_t nq) {
     const double inv = 1.0 / (double)(*S.t + 1);

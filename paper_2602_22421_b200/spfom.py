@@ -24,7 +24,7 @@ STATUS = {0: "SPFOM_OK", 1: "SPFOM_EINVAL", 2: "SPFOM_EDATA", 3: "SPFOM_ENUMERIC
 
 EXPORTED = ("spfom_workspace_bytes", "spfom_create", "spfom_step", "spfom_duals", "spfom_primal", "spfom_usage",
             "spfom_averages", "spfom_objective", "spfom_residuals", "spfom_set_state", "spfom_info",
-            "spfom_time_kernels", "spfom_step_timed", "spfom_iteration", "spfom_last_error", "spfom_destroy", "spfom_partition",
+            "spfom_time_kernels", "spfom_step_timed", "spfom_recover", "spfom_iteration", "spfom_last_error", "spfom_destroy", "spfom_partition",
             "spfom_nccl_unique_id", "spfom_build_info")
 
 
@@ -114,6 +114,7 @@ def load_library() -> C.CDLL:
         L.spfom_info.argtypes = [vp, C.POINTER(_Info)]
         L.spfom_time_kernels.argtypes = [vp, i64, vp]
         L.spfom_step_timed.argtypes = [vp, i64, vp]
+        L.spfom_recover.argtypes = [vp, vp, vp]
         L.spfom_iteration.argtypes = [vp]
         L.spfom_iteration.restype = i64
         L.spfom_last_error.argtypes = [vp]
@@ -301,6 +302,15 @@ class Solver:
         ms = np.zeros(2)
         _check(load_library().spfom_time_kernels(self._h, int(iters), ms.ctypes.data), self._h)
         return float(ms[0]), float(ms[1])
+
+    def recover(self):
+        """SBLP -> CBLP policy of the current iterate (spfom_recover): (order,
+        alpha) -- per row, product ids by y/v descending and the probabilities
+        of the nested assortments S_0..S_k (alpha row i at seg_ptr[i] + i)."""
+        order = np.empty(self.nnz, dtype=np.int32)
+        alpha = np.empty(self.nnz + self.m)
+        _check(load_library().spfom_recover(self._h, order.ctypes.data, alpha.ctypes.data), self._h)
+        return order, alpha
 
     def step_timed(self, k: int):
         """k iterations (two graph replays each) with CUDA events around the

@@ -317,3 +317,57 @@ def test_newton_budget_exhaustion_is_reported():
         gpu.duals()
     assert ei.value.status == 3
     gpu.close()
+
+
+# ------------------------------------------------------------ SBLP -> CBLP recovery
+def _check_recovery(inst, gpu, rows, exact_oracle=True):
+    """GPU recovery vs the oracle's, computed from the GPU's own iterate (same
+    u = y / v, so the order -- ties by product id -- is unique and must match
+    exactly; alpha within 1e-12), plus the policy reproducing the row."""
+    y, y0 = gpu.primal()
+    order, alpha = gpu.recover()
+    worst = 0.0
+    for i in rows:
+        sl = inst.row(int(i))
+        k = sl.stop - sl.start
+        o_pos, a_ref = oracle.recover(y0[i], y[sl], inst.attract[sl], inst.shadow[sl], inst.no_purchase[i],
+                                      inst.arrival[i], inst.prod_idx[sl])
+        got_o = order[sl]
+        got_a = alpha[sl.start + i: sl.stop + i + 1]
+        assert np.array_equal(got_o, inst.prod_idx[sl][o_pos]), (i, got_o, inst.prod_idx[sl][o_pos])
+        worst = max(worst, float(np.abs(got_a - a_ref).max()))
+        assert abs(got_a.sum() - 1.0) <= 1e-10 and got_a.min() >= -1e-12
+        pos = {int(p): q for q, p in enumerate(inst.prod_idx[sl])}
+        q0, q = oracle.policy_probabilities([pos[int(p)] for p in got_o], got_a, inst.attract[sl], inst.shadow[sl],
+                                            inst.no_purchase[i])
+        lam = inst.arrival[i]
+        assert np.abs(lam * q - y[sl]).max() <= 1e-10 * lam and abs(lam * q0 - y0[i]) <= 1e-10 * lam
+        del k
+    return worst
+
+
+@pytest.mark.parametrize("name,kw,iters", [("small", {}, 300), ("medium", dict(m=1500, N=1200, k=(20, 200)), 200),
+                                           ("tiny", {}, 50)])
+def test_recover_matches_oracle(name, kw, iters):
+    from paper_2602_22421_b200 import Solver
+    inst = generate(name, **kw)
+    gpu = Solver(inst, _params())
+    gpu.step(iters)
+    worst = _check_recovery(inst, gpu, range(inst.m))
+    gpu.close()
+    assert worst <= 1e-12, worst
+
+
+def test_recover_multi_period_and_full_size():
+    from paper_2602_22421_b200 import Solver
+    inst = generate("multi", m=600, N=500, k=(10, 120), T=3)
+    gpu = Solver(inst, _params())
+    gpu.step(60)
+    assert _check_recovery(inst, gpu, range(0, inst.m, 7)) <= 1e-12
+    gpu.close()
+    inst = generate("huge")
+    gpu = Solver(inst, _params())
+    gpu.step(5)
+    rows = np.random.default_rng(3).choice(inst.m, 300, replace=False)
+    assert _check_recovery(inst, gpu, rows) <= 1e-12
+    gpu.close()
