@@ -41,6 +41,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-iters", type=int, default=50, help="unused (kept for old command lines)")
     ap.add_argument("--cache", default=None, help="directory to cache the generated instance (npz)")
+    ap.add_argument("--mode", default="throughput", choices=["throughput", "ttg"],
+                    help="ttg: time-to-gap of the full sweep vs sampled blocks B = m/2^k (SURVEY 8(f) rank 1)")
     ap.add_argument("--stacked", action="store_true",
                     help="multi-period configs: pass the stacked instance as one period (no shared structure)")
     return ap.parse_args()
@@ -219,9 +221,54 @@ def workload_config(inst, world):
             "working set fits L2 (no flush)"}
 
 
+# --------------------------------------------------------------------- time to gap
+def run_ttg(args):
+    """Converge preset, full sweep (B = m) vs pre-generated sampled blocks
+    B = m/2, m/4, m/8: iterations and device time (CUDA events around the
+    steps only; residual checks every 50 m/B iterations are outside the timed
+    spans) until max(|rel_gap|, infeas_rel) <= 1e-3 / 1e-4 / 1e-6."""
+    import torch
+
+    from paper_2602_22421_b200 import Params, Solver
+    from spfom_inputs import block_sequence
+
+    inst = load_instance(args.config, args.cache)
+    m = inst.m
+    stream_results = []
+    for frac in (1, 2, 4, 8):
+        B = m // frac
+        blocks = None if frac == 1 else block_sequence(m, B, 512, 11)
+        s = Solver(inst, Params.converge(blocks=blocks))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dev_ms, it, hist = 0.0, 0, []
+        for _ in range(400):
+            e0.record(s.stream)
+            s.step(50 * frac)
+            e1.record(s.stream)
+            torch.cuda.synchronize()
+            dev_ms += e0.elapsed_time(e1)
+            it += 50 * frac
+            r = s.residuals()
+            hist.append((it, dev_ms, max(abs(r["rel_gap"]), r["infeas_rel"])))
+            if hist[-1][2] <= 1e-6:
+                break
+        first = lambda th: next(({"iters": i, "ms": round(t, 3)} for i, t, g in hist if g <= th), None)
+        stream_results.append({"B": B, "exec": "persistent (k_small)" if s.info()["persistent"] else "graph",
+                               "ttg_1e-3": first(1e-3), "ttg_1e-4": first(1e-4), "ttg_1e-6": first(1e-6),
+                               "final_gap": hist[-1][2], "iterations": hist[-1][0],
+                               "ms_per_iteration": hist[-1][1] / hist[-1][0]})
+        s.close()
+    print(json.dumps({"mode": "time-to-gap", "config": workload_config(inst, 1), "unit": "ms (device, CUDA events)",
+                      "preset": "converge (theta 1, tau_j 0.9/n_j, extrapolation 1)", "results": stream_results}),
+          flush=True)
+
+
 # --------------------------------------------------------------------- GPU arm
 def main():
     args = parse_args()
+    if args.mode == "ttg":
+        run_ttg(args)
+        return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -220,6 +220,7 @@ typedef struct {
     int32_t bin_G[8], bin_Q[8];
     int32_t num_bins, world;
     int64_t num_periods;              /* T (1 = single period) */
+    int64_t persistent;               /* 1: spfom_step runs the small-regime persistent kernel */
 } spfom_info_t;
 spfom_status spfom_info(const spfom_handle *h, spfom_info_t *out);
 
@@ -269,6 +270,11 @@ spfom_status spfom_partition(const int64_t *seg_ptr, int64_t num_segments, int32
 
 /* 128-byte ncclUniqueId for a new communicator (rank 0 only). */
 spfom_status spfom_nccl_unique_id(void *out128);
+
+/* sizeof of the ABI structs, for bindings to check their mirrors (host only):
+ * out[0] spfom_instance, out[1] spfom_params, out[2] spfom_info_t,
+ * out[3] spfom_residuals_t, out[4] spfom_dist. */
+void spfom_abi_sizes(size_t *out);
 
 /* Build information string (arch, version). */
 const char *spfom_build_info(void);

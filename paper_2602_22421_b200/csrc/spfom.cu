@@ -471,6 +471,14 @@ spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, in
 // ------------------------------------------------------------------ API
 extern "C" {
 
+void spfom_abi_sizes(size_t *out) {
+    out[0] = sizeof(spfom_instance);
+    out[1] = sizeof(spfom_params);
+    out[2] = sizeof(spfom_info_t);
+    out[3] = sizeof(spfom_residuals_t);
+    out[4] = sizeof(spfom_dist);
+}
+
 const char *spfom_build_info(void) {
     return "spfom-b200 0.1 (sm_100a, fp64)";
 }
@@ -1127,6 +1135,7 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
     memset(out, 0, sizeof *out);
     out->num_segments = h->m;
     out->num_periods = h->T;
+    out->persistent = h->small ? 1 : 0;
     out->num_products = h->N;
     out->nnz = h->nnz;
     out->nnz_padded = 4 * h->nq;

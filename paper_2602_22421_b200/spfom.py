@@ -25,7 +25,7 @@ STATUS = {0: "SPFOM_OK", 1: "SPFOM_EINVAL", 2: "SPFOM_EDATA", 3: "SPFOM_ENUMERIC
 EXPORTED = ("spfom_workspace_bytes", "spfom_create", "spfom_step", "spfom_duals", "spfom_primal", "spfom_usage",
             "spfom_averages", "spfom_objective", "spfom_residuals", "spfom_set_state", "spfom_info",
             "spfom_time_kernels", "spfom_step_timed", "spfom_recover", "spfom_iteration", "spfom_last_error", "spfom_destroy", "spfom_partition",
-            "spfom_nccl_unique_id", "spfom_build_info")
+            "spfom_nccl_unique_id", "spfom_build_info", "spfom_abi_sizes")
 
 
 class SpfomError(RuntimeError):
@@ -65,7 +65,7 @@ class _Info(C.Structure):
                                           "launches_per_iteration", "primal_launches_per_iteration",
                                           "workspace_bytes")] + [
         ("bin_segments", C.c_int64 * 8), ("bin_G", C.c_int32 * 8), ("bin_Q", C.c_int32 * 8),
-        ("num_bins", C.c_int32), ("world", C.c_int32), ("num_periods", C.c_int64)]
+        ("num_bins", C.c_int32), ("world", C.c_int32), ("num_periods", C.c_int64), ("persistent", C.c_int64)]
 
 
 _lib = None

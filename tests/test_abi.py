@@ -145,3 +145,14 @@ def test_product_never_imports_oracle():
             text = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"(import|from)\s+paper_2602_22421_b200", text), f
             assert '#include "spfom.h"' not in text and "spfom_kernels" not in text, f
+
+
+def test_ctypes_mirrors_match_the_header_structs(lib):
+    """The binding's ctypes structs have the C sizes (a mismatch would let the
+    library write past the Python buffers)."""
+    import ctypes as C
+    from paper_2602_22421_b200 import spfom as B
+    out = (C.c_size_t * 5)()
+    lib.spfom_abi_sizes(out)
+    assert list(out) == [C.sizeof(B._Instance), C.sizeof(B._Params), C.sizeof(B._Info), C.sizeof(B._Residuals),
+                         C.sizeof(B._Dist)]
