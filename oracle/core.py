@@ -35,7 +35,8 @@ _lp = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 class _Inst(C.Structure):
     _fields_ = [("m", C.c_int64), ("N", C.c_int64), ("seg_ptr", C.c_void_p), ("prod_idx", C.c_void_p),
                 ("v", C.c_void_p), ("w", C.c_void_p), ("v0", C.c_void_p), ("lam", C.c_void_p),
-                ("r", C.c_void_p), ("c", C.c_void_p)]
+                ("r", C.c_void_p), ("c", C.c_void_p), ("L", C.c_int64), ("bptr", C.c_void_p),
+                ("bres", C.c_void_p), ("cres", C.c_void_p)]
 
 
 class _Params(C.Structure):
@@ -78,6 +79,8 @@ def lib():
         L.oracle_dual_apply.argtypes = [C.POINTER(_Inst), C.POINTER(_Params), _dp, _dp, C.POINTER(_State)]
         L.oracle_recover.restype = None
         L.oracle_recover.argtypes = [C.c_int64, C.c_double, _dp, _dp, _dp, C.c_double, C.c_double, _ip, _lp, _dp]
+        L.oracle_prices.restype = None
+        L.oracle_prices.argtypes = [C.POINTER(_Inst), _dp, _dp]
         L.oracle_residuals.restype = C.c_int
         L.oracle_residuals.argtypes = [C.POINTER(_Inst), _dp, _dp, _dp, C.c_void_p, _dp]
         _lib = L
@@ -195,21 +198,30 @@ class OracleSolver:
             v=_f64(inst.attract), w=_f64(inst.shadow), v0=_f64(inst.no_purchase),
             lam=_f64(inst.arrival), r=_f64(inst.price), c=_f64(inst.capacity))
         k = self._keep
+        # bundles (NRM): resources of bundle j = bundle_res[bundle_ptr[j]:bundle_ptr[j+1]]
+        L = int(getattr(inst, "num_resources", 0) or 0)
+        if L > 0:
+            k.update(bptr=np.ascontiguousarray(inst.bundle_ptr, dtype=np.int64),
+                     bres=np.ascontiguousarray(inst.bundle_res, dtype=np.int32),
+                     cres=_f64(inst.resource_capacity))
+        self.L = L
         self._inst = _Inst(inst.m, inst.N, *[k[n].ctypes.data for n in
-                                             ("seg_ptr", "prod_idx", "v", "w", "v0", "lam", "r", "c")])
+                                             ("seg_ptr", "prod_idx", "v", "w", "v0", "lam", "r", "c")],
+                           L, *([k[n].ctypes.data for n in ("bptr", "bres", "cres")] if L > 0 else [None] * 3))
+        nd = L if L > 0 else inst.N              # duals: per resource (bundles) or per product
         self._params = _Params(float(theta), float(mu), float(extrapolation), int(bool(averaging)), 0,
                                int(refresh_every))
-        self.tau_j = np.zeros(inst.N)
+        self.tau_j = np.zeros(nd)
         lib().oracle_tau(C.byref(self._inst), float(tau), int(tau_mode), self.tau_j)
         self.y = np.zeros(inst.nnz)
         self.y0 = np.zeros(inst.m)
-        self.eta = np.zeros(inst.N)
+        self.eta = np.zeros(nd)
         self.s = np.zeros(inst.N)
         self.averaging = bool(averaging)
         if self.averaging:
             self.ybar = np.zeros(inst.nnz)
             self.y0bar = np.zeros(inst.m)
-            self.etabar = np.zeros(inst.N)
+            self.etabar = np.zeros(nd)
         self._state = _State(self.y.ctypes.data, self.y0.ctypes.data, self.eta.ctypes.data,
                              self.s.ctypes.data,
                              self.ybar.ctypes.data if self.averaging else None,
@@ -249,6 +261,12 @@ class OracleSolver:
     def run(self, iters: int, blocks: Optional[np.ndarray] = None) -> None:
         for t in range(iters):
             self.step(None if blocks is None else blocks[self.t % blocks.shape[0]])
+
+    def prices(self, eta=None) -> np.ndarray:
+        """g = r - A^T eta (bundles: r_j - sum_{l in B_j} eta_l)."""
+        g = np.zeros(self.inst.N)
+        lib().oracle_prices(C.byref(self._inst), _f64(self.eta if eta is None else eta), g)
+        return g
 
     def residuals(self, eta=None, y=None, y0=None) -> dict:
         out = np.zeros(len(residual_names))

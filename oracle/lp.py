@@ -189,7 +189,17 @@ def sblp_highs(inst, uncapacitated=False):
                           (np.concatenate([iy, iy]), np.concatenate([iy, iU[rows_of]]))), shape=(ny, nv))
     blocks = [r_sc]
     b_ub = [np.zeros(ny)]
-    if not uncapacitated:
+    L = int(getattr(inst, "num_resources", 0) or 0)
+    if not uncapacitated and L > 0:
+        # bundles (Eq. 33): sum_i sum_j Bt_lj y_ij <= c_l
+        bp, br = np.asarray(inst.bundle_ptr), np.asarray(inst.bundle_res)
+        nres = np.diff(bp)[inst.prod_idx]                     # resources per entry
+        rr = np.concatenate([br[bp[j]:bp[j + 1]] for j in inst.prod_idx]) if ny else np.zeros(0, int)
+        cc = np.repeat(iy, nres)
+        r_cap = sp.coo_matrix((np.ones(rr.size), (rr, cc)), shape=(L, nv))
+        blocks.append(r_cap)
+        b_ub.append(np.asarray(inst.resource_capacity, dtype=np.float64))
+    elif not uncapacitated:
         keep = np.flatnonzero(inst.present)
         pos = np.full(N, -1)
         pos[keep] = np.arange(keep.size)

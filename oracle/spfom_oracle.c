@@ -37,6 +37,12 @@
  *                    "recover", GAM reading SV App. A.1):
  *                    nested assortments by y_j / v_j descending and their
  *                    offer probabilities alpha(S_l).
+ *   bundles (NRM, Eq. 33): with L > 0 resources the
+ *                    capacity rows are sum_i sum_j Bt_lj y_ij <= c_l; prices
+ *                    g_j = r_j - sum_{l in B_j} eta_l (the Lagrangian
+ *                    coefficient), the dual step runs over resources on
+ *                    St_l = sum_{j : l in B_j} st_j, tau_l = tau / n_l with
+ *                    n_l = sum_{j : l in B_j} n_j (reading c17).
  *   oracle_residuals objective (Eq. 6), Lagrangian dual bound
  *                    D(eta) = c^T eta + sum_i lambda_i z_i(r - eta),
  *                    infeasibility, certificate (reading c11).
@@ -348,7 +354,38 @@ typedef struct {
     const int64_t *seg_ptr;
     const int32_t *prod_idx;
     const double *v, *w, *v0, *lam, *r, *c;
+    /* bundles (L > 0): resources of bundle j = bres[bptr[j] .. bptr[j+1]), capacities cres[L];
+     * eta / tau then have length L and c is unused */
+    int64_t L;
+    const int64_t *bptr;
+    const int32_t *bres;
+    const double *cres;
 } oracle_instance;
+
+static int64_t n_duals(const oracle_instance *in) { return in->L > 0 ? in->L : in->N; }
+
+/* g_j = r_j - (A^T eta)_j: eta_j per product, or sum_{l in B_j} eta_l (bundles) */
+static void prices(const oracle_instance *in, const double *eta, double *g) {
+    for (int64_t j = 0; j < in->N; ++j) {
+        if (in->L > 0) {
+            double b = 0.0;
+            for (int64_t e = in->bptr[j]; e < in->bptr[j + 1]; ++e) b += eta[in->bres[e]];
+            g[j] = in->r[j] - b;
+        } else {
+            g[j] = in->r[j] - eta[j];
+        }
+    }
+}
+
+/* public: g = r - A^T eta (test access to the effective bundle prices) */
+void oracle_prices(const oracle_instance *in, const double *eta, double *g) { prices(in, eta, g); }
+
+/* resource usage St_l = sum_{j : l in B_j} x_j (j ascending) */
+static void resource_sum(const oracle_instance *in, const double *x, double *St) {
+    for (int64_t l = 0; l < in->L; ++l) St[l] = 0.0;
+    for (int64_t j = 0; j < in->N; ++j)
+        for (int64_t e = in->bptr[j]; e < in->bptr[j + 1]; ++e) St[in->bres[e]] += x[j];
+}
 
 typedef struct {
     double theta;          /* > 0; INFINITY => exact inner argmax (Alg. 2)   */
@@ -370,8 +407,17 @@ typedef struct {
 void oracle_tau(const oracle_instance *in, double tau, int mode, double *tau_j) {
     int64_t *n = (int64_t *)calloc((size_t)in->N, sizeof(int64_t));
     for (int64_t e = 0; e < in->seg_ptr[in->m]; ++e) n[in->prod_idx[e]] += 1;
-    for (int64_t j = 0; j < in->N; ++j)
-        tau_j[j] = (mode == 1 && n[j] > 0) ? tau / (double)n[j] : tau;
+    if (in->L > 0) {               /* bundles: n_l = sum_{j : l in B_j} n_j, one tau per resource */
+        int64_t *nl = (int64_t *)calloc((size_t)in->L, sizeof(int64_t));
+        for (int64_t j = 0; j < in->N; ++j)
+            for (int64_t e = in->bptr[j]; e < in->bptr[j + 1]; ++e) nl[in->bres[e]] += n[j];
+        for (int64_t l = 0; l < in->L; ++l)
+            tau_j[l] = (mode == 1 && nl[l] > 0) ? tau / (double)nl[l] : tau;
+        free(nl);
+    } else {
+        for (int64_t j = 0; j < in->N; ++j)
+            tau_j[j] = (mode == 1 && n[j] > 0) ? tau / (double)n[j] : tau;
+    }
     free(n);
 }
 
@@ -379,11 +425,12 @@ void oracle_tau(const oracle_instance *in, double tau, int mode, double *tau_j) 
 void oracle_init(const oracle_instance *in, oracle_state *st) {
     for (int64_t e = 0; e < in->seg_ptr[in->m]; ++e) st->y[e] = 0.0;
     for (int64_t i = 0; i < in->m; ++i) st->y0[i] = in->lam[i];
-    for (int64_t j = 0; j < in->N; ++j) { st->eta[j] = 0.0; st->s[j] = 0.0; }
+    for (int64_t j = 0; j < in->N; ++j) st->s[j] = 0.0;
+    for (int64_t j = 0; j < n_duals(in); ++j) st->eta[j] = 0.0;
     if (st->ybar) {
         for (int64_t e = 0; e < in->seg_ptr[in->m]; ++e) st->ybar[e] = 0.0;
         for (int64_t i = 0; i < in->m; ++i) st->y0bar[i] = in->lam[i];
-        for (int64_t j = 0; j < in->N; ++j) st->etabar[j] = 0.0;
+        for (int64_t j = 0; j < n_duals(in); ++j) st->etabar[j] = 0.0;
     }
     st->t = 0;
 }
@@ -398,6 +445,26 @@ void oracle_dual_step(int64_t N, double *eta, const double *s_new, const double 
         double e = (1.0 - tau_j[j] * mu) * eta[j] - tau_j[j] * (c[j] - sx);
         eta[j] = e > 0.0 ? e : 0.0;
     }
+}
+
+/* Dual step of either form: per product (Eq. 17) or, with bundles, per
+ * resource on St = sum_{j in bundles(l)} (s_new + omega_x (s_new - s_old))_j. */
+static void dual_step_any(const oracle_instance *in, const oracle_params *p, const double *tau,
+                          double *eta, const double *s_new, const double *s_old) {
+    if (in->L == 0) {
+        oracle_dual_step(in->N, eta, s_new, s_old, in->c, tau, p->mu, p->extrapolation);
+        return;
+    }
+    double *sx = (double *)malloc((size_t)in->N * sizeof(double));
+    double *St = (double *)malloc((size_t)in->L * sizeof(double));
+    for (int64_t j = 0; j < in->N; ++j) sx[j] = s_new[j] + p->extrapolation * (s_new[j] - s_old[j]);
+    resource_sum(in, sx, St);
+    for (int64_t l = 0; l < in->L; ++l) {
+        double e = (1.0 - tau[l] * p->mu) * eta[l] - tau[l] * (in->cres[l] - St[l]);
+        eta[l] = e > 0.0 ? e : 0.0;
+    }
+    free(sx);
+    free(St);
 }
 
 static int update_segment(const oracle_instance *in, const oracle_params *p, const double *g,
@@ -449,7 +516,7 @@ int oracle_iterate(const oracle_instance *in, const oracle_params *p, const doub
     double *yold = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
     double *snew = (double *)malloc((size_t)N * sizeof(double));
     int rc = OR_OK;
-    for (int64_t j = 0; j < N; ++j) g[j] = in->r[j] - st->eta[j];
+    prices(in, st->eta, g);
     int full = (block == NULL || B == m);
     if (full) {
         for (int64_t i = 0; i < m && rc == OR_OK; ++i) rc = update_segment(in, p, g, i, st, zb, gb, yb);
@@ -465,14 +532,14 @@ int oracle_iterate(const oracle_instance *in, const oracle_params *p, const doub
         if (p->refresh_every > 0 && (st->t + 1) % p->refresh_every == 0) fresh_usage(in, st->y, snew);
     }
     if (rc == OR_OK) {
-        oracle_dual_step(N, st->eta, snew, st->s, in->c, tau_j, p->mu, p->extrapolation);
+        dual_step_any(in, p, tau_j, st->eta, snew, st->s);
         for (int64_t j = 0; j < N; ++j) st->s[j] = snew[j];
         st->t += 1;
         if (p->averaging && st->ybar) {
             double inv = 1.0 / (double)st->t;
             for (int64_t e = 0; e < in->seg_ptr[m]; ++e) st->ybar[e] += (st->y[e] - st->ybar[e]) * inv;
             for (int64_t i = 0; i < m; ++i) st->y0bar[i] += (st->y0[i] - st->y0bar[i]) * inv;
-            for (int64_t j = 0; j < N; ++j) st->etabar[j] += (st->eta[j] - st->etabar[j]) * inv;
+            for (int64_t j = 0; j < n_duals(in); ++j) st->etabar[j] += (st->eta[j] - st->etabar[j]) * inv;
         }
     }
     free(g); free(zb); free(gb); free(yb); free(yold); free(snew);
@@ -497,7 +564,7 @@ int oracle_primal_shard(const oracle_instance *in, const oracle_params *p, oracl
     double *gb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
     double *yb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
     int rc = OR_OK;
-    for (int64_t j = 0; j < N; ++j) g[j] = in->r[j] - st->eta[j];
+    prices(in, st->eta, g);
     for (int64_t i = 0; i < m && rc == OR_OK; ++i) rc = update_segment(in, p, g, i, st, zb, gb, yb);
     fresh_usage(in, st->y, s_local);
     free(g); free(zb); free(gb); free(yb);
@@ -506,7 +573,7 @@ int oracle_primal_shard(const oracle_instance *in, const oracle_params *p, oracl
 
 void oracle_dual_apply(const oracle_instance *in, const oracle_params *p, const double *tau_j,
                        const double *s_new, oracle_state *st) {
-    oracle_dual_step(in->N, st->eta, s_new, st->s, in->c, tau_j, p->mu, p->extrapolation);
+    dual_step_any(in, p, tau_j, st->eta, s_new, st->s);
     for (int64_t j = 0; j < in->N; ++j) st->s[j] = s_new[j];
     st->t += 1;
 }
@@ -527,6 +594,9 @@ void oracle_dual_apply(const oracle_instance *in, const oracle_params *p, const 
  * 11 cert_upper      D
  * 12 alpha
  * `present` (optional, length N) excludes products no segment considers.
+ * Bundles (L > 0): P = sum_j r_j s_j over bundles, the capacity terms (D's
+ * c^T eta, infeasibility, complementary slackness, alpha) run over resources
+ * on S_l = sum_{j : l in B_j} s_j.
  */
 int oracle_residuals(const oracle_instance *in, const double *eta, const double *y, const double *y0,
                      const uint8_t *present, double *out) {
@@ -541,21 +611,31 @@ int oracle_residuals(const oracle_instance *in, const double *eta, const double 
     double *yb = (double *)malloc((size_t)(kmax + 1) * sizeof(double));
     fresh_usage(in, y, s);
     double P = 0.0, D = 0.0, ia = 0.0, ir = 0.0, il2 = 0.0, cn2 = 0.0, cs = 0.0, alpha = 0.0;
-    for (int64_t j = 0; j < N; ++j) {
-        g[j] = in->r[j] - eta[j];
-        if (present && !present[j]) continue;
-        P += in->r[j] * s[j];
-        D += in->c[j] * eta[j];
-        double over = s[j] - in->c[j];
+    prices(in, eta, g);
+    for (int64_t j = 0; j < N; ++j)
+        if (!present || present[j]) P += in->r[j] * s[j];
+    /* capacity rows: products (c, s) or resources (cres, S = Bt s) */
+    const int64_t nr = n_duals(in);
+    double *S = s;
+    if (in->L > 0) {
+        S = (double *)malloc((size_t)in->L * sizeof(double));
+        resource_sum(in, s, S);
+    }
+    const double *cap = in->L > 0 ? in->cres : in->c;
+    for (int64_t j = 0; j < nr; ++j) {
+        if (in->L == 0 && present && !present[j]) continue;
+        D += cap[j] * eta[j];
+        double over = S[j] - cap[j];
         if (over < 0.0) over = 0.0;
         if (over > ia) ia = over;
-        double rel = over / (in->c[j] > 1.0 ? in->c[j] : 1.0);
+        double rel = over / (cap[j] > 1.0 ? cap[j] : 1.0);
         if (rel > ir) ir = rel;
         il2 += over * over;
-        cn2 += in->c[j] * in->c[j];
-        cs += eta[j] * fabs(in->c[j] - s[j]);
-        if (s[j] > 0.0 && over / s[j] > alpha) alpha = over / s[j];
+        cn2 += cap[j] * cap[j];
+        cs += eta[j] * fabs(cap[j] - S[j]);
+        if (S[j] > 0.0 && over / S[j] > alpha) alpha = over / S[j];
     }
+    if (in->L > 0) free(S);
     double bal = 0.0, scl = 0.0, neg = 0.0;
     for (int64_t i = 0; i < m; ++i) {
         int64_t a = in->seg_ptr[i], k = in->seg_ptr[i + 1] - a;

@@ -14,4 +14,5 @@ from .generate import (  # noqa: F401
     generate,
     period_slice,
     stack_periods,
+    with_bundles,
 )

@@ -78,6 +78,11 @@ class Instance:
     capacity: np.ndarray     # f64 [N]    c_j
     present: np.ndarray      # bool [N]   n_j > 0
     meta: dict
+    # bundles / NRM (Eq. 33): products are bundles over L base resources
+    num_resources: int = 0
+    bundle_ptr: Optional[np.ndarray] = None          # int64 [N+1] CSR: resources of bundle j
+    bundle_res: Optional[np.ndarray] = None          # int32 [nnz_B], strictly increasing per bundle
+    resource_capacity: Optional[np.ndarray] = None   # f64 [L]
 
     @property
     def m(self) -> int:
@@ -103,7 +108,8 @@ class Instance:
             prod_idx=self.prod_idx[a:b], attract=self.attract[a:b], shadow=self.shadow[a:b],
             no_purchase=self.no_purchase[lo:hi], arrival=self.arrival[lo:hi],
             price=self.price, capacity=self.capacity, present=self.present,
-            meta=dict(self.meta, shard=(lo, hi)))
+            meta=dict(self.meta, shard=(lo, hi)), num_resources=self.num_resources, bundle_ptr=self.bundle_ptr,
+            bundle_res=self.bundle_res, resource_capacity=self.resource_capacity)
 
 
 def _draw(rng: np.random.Generator, kind: tuple, size) -> np.ndarray:
@@ -280,7 +286,54 @@ def period_slice(inst: Instance, lo: int, hi: int) -> Instance:
     return Instance(name=f"{inst.name}[base {lo}:{hi}]", seg_ptr=seg_ptr, prod_idx=cat("prod_idx"),
                     attract=cat("attract"), shadow=cat("shadow"), no_purchase=cat("no_purchase"),
                     arrival=cat("arrival"), price=inst.price, capacity=inst.capacity, present=inst.present,
-                    meta=dict(inst.meta, T=T, m_per_period=hi - lo, shard=(lo, hi)))
+                    meta=dict(inst.meta, T=T, m_per_period=hi - lo, shard=(lo, hi)), num_resources=inst.num_resources,
+                    bundle_ptr=inst.bundle_ptr, bundle_res=inst.bundle_res, resource_capacity=inst.resource_capacity)
+
+
+def with_bundles(inst: Instance, L: Optional[int] = None, seed: int = 0, rho: float = 0.4,
+                 identity: bool = False) -> Instance:
+    """NRM bundling instance (SPEC BundleInstance S:L44-47): the
+    products of `inst` become bundles over L base resources.  Recipe: bundle j
+    consumes resource perm(j) mod L and, with probability 1/2, one more distinct
+    uniform resource (so every bundle consumes 1 or 2 resources, every resource
+    is used when L <= N); c_l = rho x sum_{j : l in B_j} d_j with d_j the
+    full-offer demand of bundle j (reading c1 applied per resource).
+    identity=True: L = N, B = I, c_l = c_j (the reduction law)."""
+    N = inst.N
+    if identity:
+        ptr = np.arange(N + 1, dtype=np.int64)
+        res = np.arange(N, dtype=np.int32)
+        return dataclasses.replace(inst, num_resources=N, bundle_ptr=ptr, bundle_res=res,
+                                   resource_capacity=np.array(inst.capacity, dtype=np.float64),
+                                   meta=dict(inst.meta, bundles="identity"))
+    L = int(L if L is not None else max(1, N // 2))
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 7717]))
+    perm = rng.permutation(N)
+    rows = []
+    for j in range(N):
+        a = int(perm[j] % L)
+        r = {a}
+        if L > 1 and rng.random() < 0.5:
+            b = int(rng.integers(0, L - 1))
+            r.add(b if b < a else b + 1)
+        rows.append(sorted(r))
+    ptr = np.zeros(N + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(r) for r in rows])
+    res = np.concatenate([np.asarray(r, dtype=np.int32) for r in rows]) if N else np.zeros(0, np.int32)
+    T = int(inst.meta.get("T", 1))
+    m1 = int(inst.meta.get("m_per_period", inst.m // T))
+    d = np.zeros(N)
+    for t in range(T):      # full-offer demand of every bundle, summed over periods
+        sub = inst.segment_slice(t * m1, (t + 1) * m1) if T > 1 else inst
+        d += _full_offer_demand(sub.seg_ptr, sub.prod_idx, sub.attract, sub.no_purchase, sub.arrival, N)
+    cres = np.zeros(L)
+    for j in range(N):
+        for l in rows[j]:
+            cres[l] += d[j]
+    cres = rho * cres
+    cres[cres <= 0] = 1.0
+    return dataclasses.replace(inst, num_resources=L, bundle_ptr=ptr, bundle_res=res, resource_capacity=cres,
+                               meta=dict(inst.meta, bundles=dict(L=L, seed=seed, rho=rho)))
 
 
 def block_sequence(m: int, B: int, iters: int, seed: int) -> np.ndarray:

@@ -1,3 +1,4 @@
+import dataclasses
 """Pins of the CPU oracle against things other than itself (all CPU, -m "not gpu").
 
 Each test names what fixes the expected value: a printed worked example
@@ -436,3 +437,65 @@ def test_recover_tie_order_by_product_index():
     y = v * 0.2                      # all ratios equal
     order, _a = oracle.recover(1.0, y, v, np.zeros(3), 1.0, 1.0 + y.sum(), np.array([7, 3, 5], np.int32))
     assert list(order) == [1, 2, 0]
+
+
+# ------------------------------------------------------------ bundles / NRM
+def test_bundle_identity_incidence_reduces_to_the_base():
+    """Reduction law: Bt = I, c_l = c_j gives the base
+    trajectory bit for bit."""
+    from spfom_inputs import with_bundles
+    inst = generate("small", m=200, N=120, k=(5, 40))
+    a = oracle.OracleSolver(inst)
+    b = oracle.OracleSolver(with_bundles(inst, identity=True))
+    for _ in range(30):
+        a.step()
+        b.step()
+    assert np.array_equal(a.y, b.y) and np.array_equal(a.y0, b.y0) and np.array_equal(a.eta, b.eta)
+    assert a.residuals() == b.residuals()
+
+
+def test_bundle_effective_coefficients_spec_example():
+    """S:L523: bundle 1 = {resources 1, 2}, eta = (0.3, 0.2), r_1 = 1 -> 0.5;
+    eta = 0 -> r (S:L524)."""
+    from spfom_inputs import with_bundles
+    inst = generate("tiny")
+    b = with_bundles(inst, identity=True)
+    ptr = np.array([0, 2] + [2 + j for j in range(1, inst.N)], dtype=np.int64)
+    res = np.array([0, 1] + [j % 2 for j in range(1, inst.N)], dtype=np.int32)
+    b = dataclasses.replace(b, num_resources=2, bundle_ptr=ptr, bundle_res=res, resource_capacity=np.ones(2),
+                            price=np.concatenate([[1.0], inst.price[1:]]))
+    S = oracle.OracleSolver(b)
+    g = S.prices(np.array([0.3, 0.2]))
+    assert abs(g[0] - 0.5) <= 1e-15
+    assert np.array_equal(S.prices(np.zeros(2)), b.price)
+
+
+def test_bundle_converges_to_the_generalized_lp_optimum():
+    """The bundle SPFOM (per-resource tau_l = 0.9 / n_l, converge preset) heads
+    to the Eq. 33 LP optimum (HiGHS on the sparse U-auxiliary form with resource
+    rows; coupled resources converge slower than the base SBLP: 1e-4 after 8000
+    iterations), and every iterate brackets it: (1 - alpha) P <= P* <= D(eta)
+    (weak duality of the bundle Lagrangian)."""
+    from oracle import lp
+    from spfom_inputs import with_bundles
+    inst = with_bundles(generate("small", m=300, N=60, k=(5, 20)), L=24, seed=3, rho=0.5)
+    Pstar, _y, _y0 = lp.sblp_highs(inst)
+    S = oracle.OracleSolver(inst)
+    for it in range(8):
+        for _ in range(1000):
+            S.step()
+        r = S.residuals()
+        assert r["cert_lower"] <= Pstar * (1 + 1e-12) and Pstar <= r["cert_upper"] * (1 + 1e-12), (it, r, Pstar)
+    assert abs(r["primal_obj"] - Pstar) <= 1e-4 * Pstar, (r["primal_obj"], Pstar)
+    assert r["infeas_rel"] <= 1e-3
+
+
+def test_bundle_infinite_capacity_keeps_resource_duals_zero():
+    """non-binding resources -> eta = 0."""
+    from spfom_inputs import with_bundles
+    inst = with_bundles(generate("small", m=100, N=40, k=(5, 20)), L=10, seed=1)
+    inst = dataclasses.replace(inst, resource_capacity=np.full(10, 1e12))
+    S = oracle.OracleSolver(inst)
+    for _ in range(20):
+        S.step()
+    assert np.all(S.eta == 0.0)
