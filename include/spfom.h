@@ -85,6 +85,15 @@ typedef enum {
  *                counts stacked segments (T x base count).  Sampled blocks are
  *                not supported with T > 1 (SPFOM_EINVAL); rows must have <= 512
  *                entries (SPFOM_EDATA).
+ *   num_resources  L; 0 = every product is its own capacity row (capacity[j]).
+ *                L > 0: bundles / NRM (Eq. 33): product j
+ *                is a bundle consuming the base resources bundle_res[bundle_ptr[j]
+ *                .. bundle_ptr[j+1]) (strictly increasing, >= 1 per bundle, < L);
+ *                the capacity rows are sum_i sum_j Bt_lj y_ij <= resource_capacity[l];
+ *                `capacity` is ignored; the duals eta (spfom_duals, set_state,
+ *                averages) are per resource (length L); prices g_j = r_j -
+ *                sum_{l in B_j} eta_l; tau_l = tau / n_l with n_l = sum_{j : l in B_j}
+ *                n_j (tau_mode 1, reading c17).
  * Violations are reported as SPFOM_EDATA.
  */
 typedef struct {
@@ -102,6 +111,10 @@ typedef struct {
     const double *price;
     const double *capacity;
     int64_t num_periods;
+    int64_t num_resources;
+    const int64_t *bundle_ptr;
+    const int32_t *bundle_res;
+    const double *resource_capacity;
 } spfom_instance;
 
 /*

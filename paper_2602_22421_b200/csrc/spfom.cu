@@ -102,7 +102,7 @@ struct Plan {
 enum Slot {
     O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
     O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
-    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_NSLOTS
+    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_NSLOTS
 };
 
 constexpr int kSpreadCopies = SPFOM_SPREAD_C;
@@ -139,9 +139,18 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_SEGC] = T * m * 16;                  // [T][m]
     sz[O_SEGV] = T * m * 32;
     sz[O_Y0BAR] = pl.averaging ? T * m * 8 : 0;
-    sz[O_R] = sz[O_C] = sz[O_TAU] = sz[O_ETA] = sz[O_G] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
+    const int64_t L = std::max<int64_t>(0, in->num_resources);
+    const int64_t D1 = std::max<int64_t>(N1, L + 1);       // duals: products or resources
+    sz[O_R] = sz[O_G] = sz[O_SCUR] = sz[O_TMP] = N1 * 8;
+    sz[O_C] = sz[O_TAU] = sz[O_ETA] = D1 * 8;
+    const int64_t nb = L > 0 ? in->bundle_ptr[pl.N] : 0;
+    sz[O_BPTR] = L > 0 ? N1 * 4 + 4 : 4;
+    sz[O_BRES] = sz[O_RBUN] = std::max<int64_t>(nb, 1) * 4;
+    sz[O_RPTR] = (L + 2) * 4;
+    sz[O_STILDE] = L > 0 ? N1 * 8 : 8;
+    sz[O_RESRES] = (size_t)kResidBlocks * 8 * 8;
     sz[O_ACC] = (spread_off(pl.N) + (size_t)kSpreadCopies * spread_range(pl.N)) * 8;   // acc, then spread copies
-    sz[O_ETABAR] = pl.averaging ? N1 * 8 : 0;
+    sz[O_ETABAR] = pl.averaging ? D1 * 8 : 0;
 
     sz[O_BLKIDS] = std::max<int64_t>(pl.block_entries, 1) * 4;
     sz[O_ROWOFF] = pl.sampled ? p->block_iters * (kNumBins + 1) * 4 : 4;
@@ -173,6 +182,8 @@ struct spfom_handle {
     char *ws = nullptr;
     DevState S;
     int64_t nq = 0, m = 0, N = 0, nnz = 0, n_present = 0, T = 1;   // base quads / segments / entries; periods
+    int64_t L = 0;                                                  // resources (bundles / NRM), 0 = none
+    std::vector<int32_t> bptr_h, bres_h;                            // relabelled bundle CSR (set_state)
     std::vector<int32_t> new2old, old2new;     // products
     std::vector<int64_t> pos_map;              // original entry -> padded entry
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
@@ -435,8 +446,17 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
     spfom_status st = allreduce(h, acc, acc, (size_t)h->N, kNcclFloat64, kNcclSum);
     if (st != SPFOM_OK) return st;
     // K3: s_new = full ? acc : s_cur + acc
-    k_dual<<<std::max<int64_t>(1, std::min<int64_t>((h->N + kThreads - 1) / kThreads, h->sm_count * 8)), kThreads, 0,
-             h->stream>>>(S, full_mode, h->pl.averaging ? 0 : 1);
+    const unsigned gN = (unsigned)std::max<int64_t>(1, std::min<int64_t>((h->N + kThreads - 1) / kThreads, h->sm_count * 8));
+    if (h->L > 0) {
+        // bundles: per-bundle usage -> per-resource dual step -> bundle prices (+ tick)
+        const unsigned gL = (unsigned)std::max<int64_t>(1, std::min<int64_t>((h->L + kThreads - 1) / kThreads, h->sm_count * 8));
+        k_bundle_usage<<<gN, kThreads, 0, h->stream>>>(S, full_mode);
+        k_bundle_dual<<<gL, kThreads, 0, h->stream>>>(S, h->pl.averaging ? 1 : 0);
+        k_bundle_prices<<<gN, kThreads, 0, h->stream>>>(S, h->pl.averaging ? 0 : 1);
+        nl += 2;
+    } else {
+        k_dual<<<gN, kThreads, 0, h->stream>>>(S, full_mode, h->pl.averaging ? 0 : 1);
+    }
     if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->T * h->nq);
     if (h->pl.averaging) k_tick<<<1, 1, 0, h->stream>>>(S.t);   // else k_dual ticks
     nl += 1 + (h->pl.averaging ? 2 : 0);
@@ -558,9 +578,28 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
             }
         }
     }
+    const int64_t L = in->num_resources;
+    if (L < 0) return fail(nullptr, SPFOM_EINVAL, "instance: num_resources must be >= 0");
     for (int64_t j = 0; j < N; ++j) {
         if (!(in->price[j] >= 0.0) || !std::isfinite(in->price[j])) { snprintf(buf, sizeof buf, "price[%lld] must be >= 0", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
-        if (!(in->capacity[j] >= 0.0) || !std::isfinite(in->capacity[j])) { snprintf(buf, sizeof buf, "capacity[%lld] must be >= 0", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
+        if (L == 0 && (!(in->capacity[j] >= 0.0) || !std::isfinite(in->capacity[j]))) { snprintf(buf, sizeof buf, "capacity[%lld] must be >= 0", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
+    }
+    if (L > 0) {
+        if (!in->bundle_ptr || !in->bundle_res || !in->resource_capacity)
+            return fail(nullptr, SPFOM_EINVAL, "instance: bundles need bundle_ptr, bundle_res, resource_capacity");
+        if (in->bundle_ptr[0] != 0) return fail(nullptr, SPFOM_EDATA, "bundle_ptr[0] must be 0");
+        if (L >= INT32_MAX) return fail(nullptr, SPFOM_EDATA, "num_resources too large");
+        for (int64_t j = 0; j < N; ++j) {
+            const int64_t a = in->bundle_ptr[j], b = in->bundle_ptr[j + 1];
+            if (b <= a) { snprintf(buf, sizeof buf, "bundle %lld consumes no resource", (long long)j); return fail(nullptr, SPFOM_EDATA, buf); }
+            for (int64_t e = a; e < b; ++e)
+                if (in->bundle_res[e] < 0 || in->bundle_res[e] >= L || (e > a && in->bundle_res[e] <= in->bundle_res[e - 1])) {
+                    snprintf(buf, sizeof buf, "bundle_res of bundle %lld out of range or not strictly increasing", (long long)j);
+                    return fail(nullptr, SPFOM_EDATA, buf);
+                }
+        }
+        for (int64_t l = 0; l < L; ++l)
+            if (!(in->resource_capacity[l] >= 0.0) || !std::isfinite(in->resource_capacity[l])) { snprintf(buf, sizeof buf, "resource_capacity[%lld] must be >= 0", (long long)l); return fail(nullptr, SPFOM_EDATA, buf); }
     }
     if (!p) return fail(nullptr, SPFOM_EINVAL, "params: NULL");
     if (!(p->theta > 0.0)) return fail(nullptr, SPFOM_EINVAL, "params: theta must be > 0 (INFINITY = exact argmax)");
@@ -659,13 +698,46 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     for (int64_t j = 0; j < N; ++j) h->n_present += counts[j] > 0;
 
     // ---- per-product arrays (relabelled), slot N = dummy
-    std::vector<double> r(N + 1, 0.0), c(N + 1, 0.0), tau(N + 1, 0.0);
+    const int64_t L = in->num_resources;
+    h->L = L;
+    const int64_t D1 = std::max<int64_t>(N + 1, L + 1);
+    std::vector<double> r(N + 1, 0.0), c(D1, 0.0), tau(D1, 0.0);
     for (int64_t jn = 0; jn < N; ++jn) {
         const int32_t jo = h->new2old[jn];
         r[jn] = in->price[jo];
+        if (L > 0) continue;
         c[jn] = in->capacity[jo];
         tau[jn] = (p->tau_mode == 1 && counts[jo] > 0) ? p->tau / (double)counts[jo] : p->tau;
         if (p->tau_mode == 1 && tau[jn] * p->mu > 1.0) { h->err = "params: tau_j * mu must be <= 1"; return bail(SPFOM_EINVAL); }
+    }
+    // bundles (NRM): relabelled CSR by bundle, CSC by resource (ascending original bundle id,
+    // the oracle's summation order), per-resource tau_l = tau / n_l, n_l = sum_{j uses l} n_j
+    std::vector<int32_t> bptr_d(N + 2, 0), bres_d, rptr_d(L + 2, 0), rbun_d;
+    if (L > 0) {
+        const int64_t nbz = in->bundle_ptr[N];
+        bres_d.resize(std::max<int64_t>(nbz, 1));
+        rbun_d.resize(std::max<int64_t>(nbz, 1));
+        for (int64_t jn = 0; jn < N; ++jn) {
+            const int32_t jo = h->new2old[jn];
+            bptr_d[jn + 1] = bptr_d[jn] + (int32_t)(in->bundle_ptr[jo + 1] - in->bundle_ptr[jo]);
+            for (int64_t e = in->bundle_ptr[jo]; e < in->bundle_ptr[jo + 1]; ++e)
+                bres_d[bptr_d[jn] + (e - in->bundle_ptr[jo])] = in->bundle_res[e];
+        }
+        std::vector<int64_t> nl(L, 0);
+        for (int64_t e = 0; e < nbz; ++e) rptr_d[in->bundle_res[e] + 1] += 1;
+        for (int64_t l = 0; l < L; ++l) rptr_d[l + 1] += rptr_d[l];
+        std::vector<int32_t> fill(rptr_d.begin(), rptr_d.end() - 1);
+        for (int64_t jo = 0; jo < N; ++jo)                       // ascending original bundle id
+            for (int64_t e = in->bundle_ptr[jo]; e < in->bundle_ptr[jo + 1]; ++e) {
+                const int32_t l = in->bundle_res[e];
+                rbun_d[fill[l]++] = h->old2new[jo];
+                nl[l] += counts[jo];
+            }
+        for (int64_t l = 0; l < L; ++l) {
+            c[l] = in->resource_capacity[l];
+            tau[l] = (p->tau_mode == 1 && nl[l] > 0) ? p->tau / (double)nl[l] : p->tau;
+            if (p->tau_mode == 1 && tau[l] * p->mu > 1.0) { h->err = "params: tau_l * mu must be <= 1"; return bail(SPFOM_EINVAL); }
+        }
     }
 
     // ---- length bins; device segment order = (bin, local id), so that every
@@ -775,14 +847,19 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     for (int64_t k = 0; k < T * m; ++k) y0[k] = segv[k].x;
     bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
               H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
-              H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), (N + 1) * 8) &&
-              H2D(O_TAU, tau.data(), (N + 1) * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
+              H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), D1 * 8) &&
+              H2D(O_TAU, tau.data(), D1 * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
               H2D(O_ORIG, h->new2old.data(), N * 4);
+    h->bptr_h = bptr_d;
+    h->bres_h = bres_d;
+    if (L > 0)
+        ok = ok && H2D(O_BPTR, bptr_d.data(), (N + 1) * 4) && H2D(O_BRES, bres_d.data(), bres_d.size() * 4) &&
+             H2D(O_RPTR, rptr_d.data(), (L + 1) * 4) && H2D(O_RBUN, rbun_d.data(), rbun_d.size() * 4);
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
-    ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, (N + 1) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
+    ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, D1 * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
          Z(O_COUNTERS, 64) && Z(O_T, 8);
-    if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, (N + 1) * 8);
+    if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, D1 * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
 
@@ -802,6 +879,12 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.eta = slot_ptr<double>(h, O_ETA);
     S.g = slot_ptr<double>(h, O_G);
     S.s = slot_ptr<double>(h, O_ACC);
+    S.L = (int32_t)L;
+    S.bptr = slot_ptr<int32_t>(h, O_BPTR);
+    S.bres = slot_ptr<int32_t>(h, O_BRES);
+    S.rptr = slot_ptr<int32_t>(h, O_RPTR);
+    S.rbun = slot_ptr<int32_t>(h, O_RBUN);
+    S.stilde = slot_ptr<double>(h, O_STILDE);
     S.spread_off = (int32_t)spread_off(N);
     S.spread = S.s + S.spread_off;
     S.spread_n = (int32_t)spread_range(N);
@@ -826,7 +909,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         int64_t max_rq = 0;
         for (int64_t k = 0; k < m; ++k) max_rq = std::max<int64_t>(max_rq, qoff[k + 1] - qoff[k]);
         const int64_t per_iter = pl.sampled ? p->block_size : m;
-        const bool eligible = h->world == 1 && T == 1 && !pl.averaging && !(pl.sampled && p->refresh_every > 0) &&
+        const bool eligible = h->world == 1 && T == 1 && h->L == 0 && !pl.averaging && !(pl.sampled && p->refresh_every > 0) &&
                               max_rq <= 256 && per_iter <= 4096;
         if (p->exec_mode == 2 && !eligible) {
             h->err = "exec_mode 2 needs world == 1, T == 1, no averaging/refresh, rows <= 1024 entries, <= 4096 segments per iteration";
@@ -956,13 +1039,24 @@ static spfom_status check_counters(spfom_handle *h) {
     return SPFOM_OK;
 }
 
-spfom_status spfom_duals(spfom_handle *h, double *eta) {
-    if (!h || !eta) return SPFOM_EINVAL;
+// duals in caller order: products (original ids) or, with bundles, resources (not relabelled)
+static spfom_status fetch_duals(spfom_handle *h, const double *src, double *eta) {
+    if (h->L > 0) {
+        CUDA_TRY(h, cudaMemcpyAsync(eta, src, h->L * 8, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        return SPFOM_OK;
+    }
     std::vector<double> tmp(h->N);
-    CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.eta, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), src, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     for (int64_t jn = 0; jn < h->N; ++jn) eta[h->new2old[jn]] = tmp[jn];
-    return check_counters(h);
+    return SPFOM_OK;
+}
+
+spfom_status spfom_duals(spfom_handle *h, double *eta) {
+    if (!h || !eta) return SPFOM_EINVAL;
+    spfom_status st = fetch_duals(h, h->S.eta, eta);
+    return st != SPFOM_OK ? st : check_counters(h);
 }
 
 spfom_status spfom_usage(spfom_handle *h, double *s) {
@@ -1004,12 +1098,7 @@ spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double
     if (!h->pl.averaging) return fail(h, SPFOM_EINVAL, "averaging is off");
     spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, 8, ybar, y0bar);
     if (st != SPFOM_OK) return st;
-    if (etabar) {
-        std::vector<double> tmp(h->N);
-        CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.etabar, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        for (int64_t jn = 0; jn < h->N; ++jn) etabar[h->new2old[jn]] = tmp[jn];
-    }
+    if (etabar) return fetch_duals(h, h->S.etabar, etabar);
     return SPFOM_OK;
 }
 
@@ -1035,12 +1124,16 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     }
     double *pprod = slot_ptr<double>(h, O_RESPROD);
     k_resid_prod<<<kResidBlocks, kThreads, 0, h->stream>>>(S, sf, h->n_present, pprod);
+    double *pres = slot_ptr<double>(h, O_RESRES);
+    if (h->L > 0) k_resid_res<<<kResidBlocks, kThreads, 0, h->stream>>>(S, sf, pres);   // resource rows
     CUDA_TRY(h, cudaGetLastError());
     // cross-rank: sum of D_seg, max of the audits (local segment quantities)
     double *red = slot_ptr<double>(h, O_COUNTS);   // reuse the counts slot as scratch (>= 4 doubles)
     std::vector<double> hs((size_t)kNumBins * kResidBlocks * 4), hp((size_t)kResidBlocks * 8);
     CUDA_TRY(h, cudaMemcpyAsync(hs.data(), pseg, hs.size() * 8, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaMemcpyAsync(hp.data(), pprod, hp.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    std::vector<double> hr(h->L > 0 ? hp.size() : 0);
+    if (h->L > 0) CUDA_TRY(h, cudaMemcpyAsync(hr.data(), pres, hr.size() * 8, cudaMemcpyDeviceToHost, h->stream));
     unsigned long long cnt[3];
     CUDA_TRY(h, cudaMemcpyAsync(cnt, h->S.counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1053,6 +1146,9 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     for (int b = 0; b < kResidBlocks; ++b)
         for (int k = 0; k < 8; ++k)
             pr[k] = (k == 2 || k == 3 || k == 7) ? std::max(pr[k], hp[8 * b + k]) : pr[k] + hp[8 * b + k];
+    for (size_t b = 0; b < hr.size() / 8; ++b)      // bundles: the capacity rows are resources
+        for (int k = 0; k < 8; ++k)
+            pr[k] = (k == 2 || k == 3 || k == 7) ? std::max(pr[k], hr[8 * b + k]) : pr[k] + hr[8 * b + k];
     if (h->world > 1) {
         double buf[4] = {dseg, agg[0], agg[1], agg[2]};
         CUDA_TRY(h, cudaMemcpyAsync(red, buf, 32, cudaMemcpyHostToDevice, h->stream));
@@ -1110,13 +1206,23 @@ spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0,
                                       cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
-    std::vector<double> t1(h->N + 1, 0.0), t2(h->N + 1, 0.0);
+    std::vector<double> t1(std::max<int64_t>(h->N, h->L) + 1, 0.0), t2(h->N + 1, 0.0);
     if (eta) {
         std::vector<double> r(h->N + 1, 0.0);
         CUDA_TRY(h, cudaMemcpyAsync(r.data(), h->S.r, (h->N + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-        for (int64_t jn = 0; jn < h->N; ++jn) { t1[jn] = eta[h->new2old[jn]]; t2[jn] = r[jn] - t1[jn]; }
-        CUDA_TRY(h, cudaMemcpyAsync(h->S.eta, t1.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+        if (h->L > 0) {
+            // resource duals as given; bundle prices g_j = r_j - sum_{l in B_j} eta_l
+            for (int64_t l = 0; l < h->L; ++l) t1[l] = eta[l];
+            for (int64_t jn = 0; jn < h->N; ++jn) {
+                double b = 0.0;
+                for (int32_t e = h->bptr_h[jn]; e < h->bptr_h[jn + 1]; ++e) b += eta[h->bres_h[e]];
+                t2[jn] = r[jn] - b;
+            }
+        } else {
+            for (int64_t jn = 0; jn < h->N; ++jn) { t1[jn] = eta[h->new2old[jn]]; t2[jn] = r[jn] - t1[jn]; }
+        }
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.eta, t1.data(), t1.size() * 8, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaMemcpyAsync(h->S.g, t2.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     }
@@ -1152,7 +1258,8 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
     }
     out->primal_launches_per_iteration = np;
     // primal launches + K3 (+ k_average + k_tick with averaging) (+ k_fold when world > 1)
-    out->launches_per_iteration = np + 1 + (h->pl.averaging ? 2 : 0) + (h->world > 1 && h->S.spread_n > 0 ? 1 : 0);
+    out->launches_per_iteration = np + 1 + (h->pl.averaging ? 2 : 0) + (h->world > 1 && h->S.spread_n > 0 ? 1 : 0) +
+                                  (h->L > 0 ? 2 : 0);
     return SPFOM_OK;
 }
 

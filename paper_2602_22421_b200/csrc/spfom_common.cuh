@@ -40,6 +40,12 @@ struct DevState {
     // products [hh, spread_n) reduce into spread[c * spread_n + j], c = warp % spread_c,
     // so that no single address takes every segment's update; folded into s
     // by K3 (world == 1) or k_fold before the allreduce
+    // bundles / NRM (L > 0): eta, c, tau, etabar hold the L resources; bundle j
+    // (relabelled) consumes bres[bptr[j] .. bptr[j+1]); resource l is used by
+    // the bundles rbun[rptr[l] .. rptr[l+1]) (ascending original bundle id)
+    int32_t L;
+    const int32_t *bptr, *bres, *rptr, *rbun;
+    double *stilde;                // [N + 1] extrapolated bundle usage of the iteration
     double *spread;                // = s + spread_off
     int32_t spread_n, spread_c, spread_off;
     int32_t fold_in_dual;

@@ -23,6 +23,20 @@ namespace spfom {
 // acc = 0.  a8 (averaging): etabar += (eta - etabar) / t.
 // tick != 0 (no averaging): the last block to finish also advances the
 // iteration counter (one launch less per iteration than a separate k_tick).
+__global__ void k_tick(int64_t *t) { *t += 1; }
+
+// last block of a grid advances the iteration counter (fused tick)
+__device__ __forceinline__ void tick_last_block(const DevState &S) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(S.counters + 3, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+            *S.t += 1;
+            S.counters[3] = 0;
+        }
+    }
+}
+
 // a7 for one product j (Eq. 17 with extrapolation and per-product tau_j)
 __device__ __forceinline__ void dual_update(const DevState &S, int64_t j, int32_t full, int64_t t_next) {
     double acc = S.s[j];
@@ -47,19 +61,87 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int
     const int64_t t_next = tick ? 0 : *S.t + 1;     // t is only needed for averaging (tick == 0)
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x)
         dual_update(S, j, full, t_next);
-    if (tick) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(S.counters + 3, 1ull) == (unsigned long long)gridDim.x - 1ull) {
-                *S.t += 1;
-                S.counters[3] = 0;
-            }
-        }
-    }
+    if (tick) tick_last_block(S);
 }
 
-__global__ void k_tick(int64_t *t) { *t += 1; }
+// ----------------------------------------------------------------- bundles (a7, NRM)
+// P:L719-741 Eq. 33: the dual step runs over the L resources.
+// 1) per bundle: s_new, st = s_new + omega_x (s_new - s_prev), s_prev = s_new
+__global__ void __launch_bounds__(kThreads) k_bundle_usage(DevState S, int32_t full) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
+        double acc = S.s[j];
+        if (S.fold_in_dual && j < S.spread_n) {
+            for (int c = 0; c < S.spread_c; ++c) {
+                acc += S.spread[(size_t)c * S.spread_n + j];
+                S.spread[(size_t)c * S.spread_n + j] = 0.0;
+            }
+        }
+        const double sn = full ? acc : S.s_prev[j] + acc;
+        S.stilde[j] = fma(S.omega_x, sn - S.s_prev[j], sn);
+        S.s_prev[j] = sn;
+        S.s[j] = 0.0;
+    }
+}
+// 2) per resource: St_l = sum_{j uses l} st_j (ascending original bundle id),
+//    eta_l = max{0, (1 - tau_l mu) eta_l - tau_l (c_l - St_l)}
+__global__ void __launch_bounds__(kThreads) k_bundle_dual(DevState S, int32_t averaging) {
+    const int64_t t_next = averaging ? *S.t + 1 : 0;
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < S.L; l += (int64_t)gridDim.x * blockDim.x) {
+        double st = 0.0;
+        for (int32_t e = S.rptr[l]; e < S.rptr[l + 1]; ++e) st += S.stilde[S.rbun[e]];
+        const double tl = S.tau[l];
+        const double e = fmax(0.0, fma(-tl, S.c[l] - st, (1.0 - tl * S.mu) * S.eta[l]));
+        S.eta[l] = e;
+        if (S.etabar) S.etabar[l] += (e - S.etabar[l]) / (double)t_next;
+    }
+}
+// 3) per bundle: g_j = r_j - sum_{l in B_j} eta_l; optional tick
+__global__ void __launch_bounds__(kThreads) k_bundle_prices(DevState S, int32_t tick) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
+        double b = 0.0;
+        for (int32_t e = S.bptr[j]; e < S.bptr[j + 1]; ++e) b += S.eta[S.bres[e]];
+        S.g[j] = S.r[j] - b;
+    }
+    if (tick) tick_last_block(S);
+}
+
+// Residual terms of the resource rows (bundles): partials[8] per block as in
+// k_resid_prod with slot 0 (objective) left 0.
+__global__ void __launch_bounds__(kThreads) k_resid_res(DevState S, const double *sfresh, double *partials) {
+    __shared__ double red[kThreads / 32][8];
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < S.L; l += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int32_t e = S.rptr[l]; e < S.rptr[l + 1]; ++e) s += sfresh[S.rbun[e]];
+        const double c = S.c[l], et = S.eta[l];
+        const double over = fmax(0.0, s - c);
+        acc[1] += c * et;
+        acc[2] = fmax(acc[2], over);
+        acc[3] = fmax(acc[3], over / fmax(1.0, c));
+        acc[4] += over * over;
+        acc[5] += c * c;
+        acc[6] += et * fabs(c - s);
+        if (s > 0.0) acc[7] = fmax(acc[7], over / s);
+    }
+    const int lane = threadIdx.x & 31;
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double other = __shfl_xor_sync(0xffffffffu, acc[k], o);
+            acc[k] = (k == 2 || k == 3 || k == 7) ? fmax(acc[k], other) : acc[k] + other;
+        }
+    }
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) red[threadIdx.x / 32][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < kThreads / 32; ++w)
+            for (int k = 0; k < 8; ++k)
+                out[k] = (k == 2 || k == 3 || k == 7) ? fmax(out[k], red[w][k]) : out[k] + red[w][k];
+        for (int k = 0; k < 8; ++k) partials[8 * blockIdx.x + k] = out[k];
+    }
+}
 
 // world > 1: fold K1's spread copies into the usage accumulator before the allreduce
 __global__ void __launch_bounds__(kThreads) k_fold(DevState S) {
@@ -423,9 +505,11 @@ __global__ void __launch_bounds__(kThreads) k_resid_prod(DevState S, const doubl
     __shared__ double red[kThreads / 32][8];
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_present; j += (int64_t)gridDim.x * blockDim.x) {
-        const double s = sfresh[j], c = S.c[j], e = S.eta[j];
-        const double over = fmax(0.0, s - c);
+        const double s = sfresh[j];
         acc[0] += S.r[j] * s;
+        if (S.L > 0) continue;                 // bundles: capacity rows are resources (k_resid_res)
+        const double c = S.c[j], e = S.eta[j];
+        const double over = fmax(0.0, s - c);
         acc[1] += c * e;
         acc[2] = fmax(acc[2], over);
         acc[3] = fmax(acc[3], over / fmax(1.0, c));

@@ -39,7 +39,9 @@ class _Instance(C.Structure):
                 ("segment_offset", C.c_int64), ("num_segments_global", C.c_int64),
                 ("seg_ptr", C.c_void_p), ("prod_idx", C.c_void_p), ("attract", C.c_void_p),
                 ("shadow", C.c_void_p), ("no_purchase", C.c_void_p), ("arrival", C.c_void_p),
-                ("price", C.c_void_p), ("capacity", C.c_void_p), ("num_periods", C.c_int64)]
+                ("price", C.c_void_p), ("capacity", C.c_void_p), ("num_periods", C.c_int64),
+                ("num_resources", C.c_int64), ("bundle_ptr", C.c_void_p), ("bundle_res", C.c_void_p),
+                ("resource_capacity", C.c_void_p)]
 
 
 class _Params(C.Structure):
@@ -222,11 +224,20 @@ class Solver:
         self.m = mb * self.periods            # stacked sizes: the getters' shapes
         self.N = k["price"].shape[0]
         self.nnz = nb * self.periods
+        # bundles / NRM: duals per resource
+        self.L = int(getattr(inst, "num_resources", 0) or 0)
+        if self.L > 0:
+            k.update(bundle_ptr=np.ascontiguousarray(inst.bundle_ptr, dtype=np.int64),
+                     bundle_res=np.ascontiguousarray(inst.bundle_res, dtype=np.int32),
+                     resource_capacity=_f64(inst.resource_capacity))
+        self.n_duals = self.L if self.L > 0 else self.N
         self._inst = _Instance(mb, self.N, nb, int(segment_offset),
                                int(num_segments_global if num_segments_global is not None else mb),
                                *[k[n].ctypes.data for n in ("seg_ptr", "prod_idx", "attract", "shadow",
                                                             "no_purchase", "arrival", "price", "capacity")],
-                               self.periods)
+                               self.periods, self.L,
+                               *([k[n].ctypes.data for n in ("bundle_ptr", "bundle_res", "resource_capacity")]
+                                 if self.L > 0 else [None] * 3))
         self._params, self._blocks = self.params._c()
         nbytes = C.c_size_t()
         _check(L.spfom_workspace_bytes(C.byref(self._inst), C.byref(self._params), C.byref(nbytes)))
@@ -256,7 +267,7 @@ class Solver:
         _check(load_library().spfom_step(self._h, int(k)), self._h)
 
     def duals(self) -> np.ndarray:
-        out = np.empty(self.N)
+        out = np.empty(self.n_duals)
         _check(load_library().spfom_duals(self._h, out.ctypes.data), self._h)
         return out
 
@@ -271,7 +282,7 @@ class Solver:
         return out
 
     def averages(self):
-        y, y0, e = np.empty(self.nnz), np.empty(self.m), np.empty(self.N)
+        y, y0, e = np.empty(self.nnz), np.empty(self.m), np.empty(self.n_duals)
         _check(load_library().spfom_averages(self._h, y.ctypes.data, y0.ctypes.data, e.ctypes.data), self._h)
         return y, y0, e
 

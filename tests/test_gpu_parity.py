@@ -371,3 +371,41 @@ def test_recover_multi_period_and_full_size():
     rows = np.random.default_rng(3).choice(inst.m, 300, replace=False)
     assert _check_recovery(inst, gpu, rows) <= 1e-12
     gpu.close()
+
+
+# ------------------------------------------------------------ bundles / NRM (Eq. 33)
+@pytest.mark.parametrize("name,kw,L,blocks_B", [
+    ("small", dict(m=400, N=120, k=(5, 40)), 40, None),
+    ("medium", dict(m=2000, N=1500, k=(20, 200)), 500, None),        # several bins, Zipf head
+    ("small", dict(m=600, N=200, k=(5, 40)), 64, 150),               # sampled blocks
+    ("multi", dict(m=300, N=200, k=(5, 60), T=3), 70, None),         # shared periods
+])
+def test_bundle_lockstep_100(name, kw, L, blocks_B):
+    from spfom_inputs import with_bundles
+    inst = with_bundles(generate(name, **kw), L=L, seed=2)
+    blocks = None if blocks_B is None else block_sequence(inst.m, blocks_B, 32, 5)
+    worst, gpu, cpu = lockstep(inst, _params(blocks=blocks), 100, blocks=blocks)
+    assert gpu.duals().shape == (L,)
+    rg, ro = gpu.residuals(), cpu.residuals()
+    gpu.close()
+    _assert_ok(worst)
+    for k in ("primal_obj", "dual_obj", "cert_lower", "cert_upper"):
+        assert abs(rg[k] - ro[k]) <= 1e-10 * abs(ro[k]), (k, rg[k], ro[k])
+    for k in ("infeas_abs", "infeas_rel", "alpha", "compl_slack"):
+        assert abs(rg[k] - ro[k]) <= 1e-10 * max(1.0, abs(ro[k])), (k, rg[k], ro[k])
+
+
+def test_bundle_identity_incidence_equals_plain_path():
+    """Reduction law on the GPU: Bt = I runs the bundle dual kernels
+    yet reproduces the per-product path."""
+    from paper_2602_22421_b200 import Solver
+    from spfom_inputs import with_bundles
+    inst = generate("medium", m=1500, N=900, k=(20, 120))
+    a, b = Solver(inst, _params(exec_mode=1)), Solver(with_bundles(inst, identity=True), _params())
+    a.step(40)
+    b.step(40)
+    ya, _ = a.primal()
+    yb, _ = b.primal()
+    assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
