@@ -370,7 +370,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
     const bool argmax = std::isinf(h->params.theta);
     DevState S = h->S;
     int64_t nl = 0;
-    const bool fork = !h->pl.sampled && h->nbins_active > 1;
+    const bool fork = h->nbins_active > 1;
     if (fork) {
         CUDA_TRY(h, cudaEventRecord(h->ev_fork, h->stream));
         for (int b = 0; b < kNumBins; ++b)
@@ -409,7 +409,8 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             maxc = cnt;
         }
         if (maxc == 0) continue;
-        primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, h->sm_count, h->stream);
+        primal_dispatch(b, argmax, h->pl.sampled, S, L, maxc, fork ? h->bin_sms[b] : h->sm_count,
+                        fork ? h->side[b] : h->stream);
         ++nl;
     }
     if (fork) {
@@ -938,18 +939,21 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             }
         }
     }
-    // full sweep over several bins: SM shares proportional to each bin's padded entries
-    if (!pl.sampled) {
+    // several active bins: concurrent launches on SM shares proportional to each bin's work
+    // (full sweep: padded entries; sampled: the largest per-iteration count x capacity)
+    if (!h->small) {
         int64_t wtot = 0, w[kNumBins] = {0};
         for (int b = 0; b < kNumBins; ++b) {
-            w[b] = (int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + (h->bin_first[b + 1] - h->bin_first[b]);
-            if (h->bin_first[b + 1] > h->bin_first[b]) h->nbins_active += 1;
+            const int64_t cnt = pl.sampled ? h->pl.bin_count[b] : (h->bin_first[b + 1] - h->bin_first[b]);
+            w[b] = pl.sampled ? cnt * (int64_t)kBins[b].G * kBins[b].Q
+                              : (int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt;
+            if (cnt > 0) h->nbins_active += 1;
             wtot += w[b];
         }
         if (h->nbins_active > 1) {
             bool okc = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) == cudaSuccess;
             for (int b = 0; b < kNumBins && okc; ++b) {
-                if (h->bin_first[b + 1] == h->bin_first[b]) continue;
+                if (w[b] == 0) continue;
                 h->bin_sms[b] = (int)std::max<int64_t>(1, (int64_t)((double)h->sm_count * (double)w[b] / (double)std::max<int64_t>(wtot, 1) + 0.5));
                 okc = cudaStreamCreateWithFlags(&h->side[b], cudaStreamNonBlocking) == cudaSuccess &&
                       cudaEventCreateWithFlags(&h->ev_join[b], cudaEventDisableTiming) == cudaSuccess;

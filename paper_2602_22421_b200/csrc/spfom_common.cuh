@@ -189,6 +189,26 @@ __device__ __forceinline__ bool seg_slot(const SegList &L, const DevState &S, in
     return true;
 }
 
+// The launch's segment list resolved once: ids (null = contiguous from first) and count.
+struct SegSpan {
+    const int32_t *ids;
+    int64_t first, count;
+};
+__device__ __forceinline__ SegSpan seg_span(const SegList &L, const DevState &S) {
+    if (L.row_off) {
+        const int64_t row = (*S.t) % L.block_iters;
+        const int32_t *ro = L.row_off + row * (L.nbins + 1);
+        const int64_t a = ro[L.bin], b = ro[L.bin + 1];
+        return SegSpan{L.ids + a, 0, b - a};
+    }
+    return SegSpan{L.ids ? L.ids + L.first : nullptr, L.ids ? 0 : L.first, L.count};
+}
+__device__ __forceinline__ bool span_slot(const SegSpan &P, int64_t slot, int64_t &i) {
+    if (slot >= P.count) return false;
+    i = P.ids ? (int64_t)P.ids[slot] : P.first + slot;
+    return true;
+}
+
 __device__ __forceinline__ int64_t seg_count(const SegList &L, const DevState &S) {
     if (L.row_off) {
         const int64_t row = (*S.t) % L.block_iters;

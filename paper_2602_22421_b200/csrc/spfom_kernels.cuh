@@ -408,13 +408,14 @@ __global__ void __launch_bounds__(kThreads) k_resid_seg(DevState S, SegList L, d
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const int64_t groups_per_block = (int64_t)kThreads / G;
-    const int64_t total = seg_count(L, S);
+    const SegSpan span = seg_span(L, S);
+    const int64_t total = span.count;
     const int64_t stride = (int64_t)gridDim.x * groups_per_block;
     const int64_t slot_end = ((total + stride - 1) / stride) * stride;
     double dsum = 0.0, bmax = 0.0, smax = 0.0, nmax = 0.0;
     for (int64_t slot = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; slot < slot_end; slot += stride) {
         int64_t i = 0;
-        const bool active = seg_slot(L, S, slot, i);
+        const bool active = span_slot(span, slot, i);
         double lam = 1.0, vt0 = 1.0, y0 = 1.0;
         int32_t q0 = 0, q1 = 0;
         if (active) {

@@ -896,14 +896,15 @@ __global__ void __launch_bounds__(kPrimalThreads, list_min_blocks<Q>()) k_primal
     double *hg = sm.hist + (warp * GPW + gidx) * HS;
 
     const int64_t groups_per_block = kPrimalThreads / G;
-    const int64_t total = seg_count(L, S);
+    const SegSpan span = seg_span(L, S);              // row of the block table resolved once
+    const int64_t total = span.count;
     const int64_t stride = (int64_t)gridDim.x * groups_per_block;
     const int64_t slot_end = ((total + stride - 1) / stride) * stride;   // warp-uniform trip count
     ProjStats st;
 
     for (int64_t slot = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; slot < slot_end; slot += stride) {
         int64_t i = 0;
-        const bool active = seg_slot(L, S, slot, i);
+        const bool active = span_slot(span, slot, i);
 
         // ---- segment state and this lane's quads
         double lam = 1.0, vt0 = 1.0;
