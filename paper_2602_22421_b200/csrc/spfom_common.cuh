@@ -7,6 +7,10 @@
 
 #include <type_traits>
 
+#ifndef SPFOM_L2_HINTS
+#define SPFOM_L2_HINTS 1
+#endif
+
 namespace spfom {
 
 constexpr int kThreads = 256;       // non-primal kernels
@@ -112,6 +116,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// L2 evict-first policy for data streamed once per iteration (keeps g, the
+// usage accumulators and the per-segment state resident in L2)
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+#if SPFOM_L2_HINTS
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+#else
+    (void)pol;
+    bulk_g2s(dst, src, bytes, bar);
+#endif
+}
+__device__ __forceinline__ void st256_stream(double *p, double a, double b, double c, double d) {
+#if SPFOM_L2_HINTS
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+#else
+    st256(p, a, b, c, d);
+#endif
 }
 
 // TMA bulk prefetch of a contiguous range into L2 (bytes: multiple of 16, 16-B aligned)

@@ -315,14 +315,17 @@ __device__ __forceinline__ void argmax_group(const double (&g)[NE], const double
 
 // a5, one group: head entries into the group's private histogram, tail
 // entries (and no pads: pads carry id N) into s by fp64 reductions.
+// Warm head [HH, spread_n) goes to this warp's spread copy (offset spread_rel
+// from s), the rest of the tail to s itself.
 template <int NE>
 __device__ __forceinline__ void scatter_group(const int (&idx)[NE], const double (&c)[NE], double *hg, int HH,
-                                              double *s, int N) {
+                                              double *s, int N, int spread_n, int spread_rel) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
         const int j = idx[e];
         if (j < HH) hg[j] += c[e];
-        red_add_if(s + j, c[e], j >= HH && j < N);
+        const int off = j < spread_n ? spread_rel + j : j;
+        red_add_if(s + off, c[e], j >= HH && j < N);
     }
 }
 
@@ -469,10 +472,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
             bulk_g2s(slot + LY::OFF_SEGC, S.segc + s0, 16u * n, bar);
             if (wbytes) bulk_g2s(slot + LY::OFF_QW, S.qoff + w0, wbytes, bar);
             if (nq > 0) {
-                bulk_g2s(slot + LY::OFF_IDS, S.pidx + qa, 16u * nq, bar);
-                bulk_g2s(slot + LY::OFF_V, S.v + 4 * (int64_t)qa, 32u * nq, bar);
-                bulk_g2s(slot + LY::OFF_OM, S.om + 4 * (int64_t)qa, 32u * nq, bar);
-                bulk_g2s(slot + LY::OFF_Y, S.y + 4 * (int64_t)qa, 32u * nq, bar);
+                const uint64_t pol = l2_evict_first_policy();
+                bulk_g2s_hint(slot + LY::OFF_IDS, S.pidx + qa, 16u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_V, S.v + 4 * (int64_t)qa, 32u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_OM, S.om + 4 * (int64_t)qa, 32u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_Y, S.y + 4 * (int64_t)qa, 32u * nq, bar, pol);
             }
         }
     };
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
 #pragma unroll
         for (int t = 0; t < Q; ++t) {
             const int32_t q = qa + gl + G * t;
-            if (q < qb) st256(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
+            if (q < qb) st256_stream(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
         // a5: head -> histogram, warm head -> spread copies, tail -> s
@@ -894,6 +898,9 @@ __global__ void __launch_bounds__(kPrimalThreads, list_min_blocks<Q>()) k_primal
     for (int j = threadIdx.x; j < WARPS * GPW * HS; j += kPrimalThreads) sm.hist[j] = 0.0;
     __syncthreads();
     double *hg = sm.hist + (warp * GPW + gidx) * HS;
+    const int spread_n = S.spread_n;
+    const int spread_rel = S.spread_off +
+        (int)((((int64_t)blockIdx.x * WARPS + warp)) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
     const int64_t groups_per_block = kPrimalThreads / G;
     const SegSpan span = seg_span(L, S);              // row of the block table resolved once
@@ -972,7 +979,7 @@ __global__ void __launch_bounds__(kPrimalThreads, list_min_blocks<Q>()) k_primal
 #pragma unroll
             for (int e = 0; e < NE; ++e) yv[e] -= yold[e];
         }
-        scatter_group<NE>(idx, yv, hg, HH, S.s, N);
+        scatter_group<NE>(idx, yv, hg, HH, S.s, N, spread_n, spread_rel);
     }
     if constexpr (!ARGMAX) {
         if (st.passes) {
