@@ -26,31 +26,50 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, errq):
+def _worker(rank, world, port, errq, variant="plain"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import oracle
         from paper_2602_22421_b200 import partition
-        from spfom_inputs import generate
+        from spfom_inputs import generate, period_slice, with_bundles
 
-        inst = generate("medium", m=900, N=300, k=(20, 80))
-        bounds = partition(inst.seg_ptr, world)
-        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-        shard = inst.segment_slice(lo, hi)
+        if variant == "multi":
+            # shared-structure multi-period: ranks own whole base segments (all T periods)
+            inst = generate("multi", m=300, N=200, k=(10, 60), T=3)
+            T, mb = 3, 300
+            bounds = partition(inst.seg_ptr[: mb + 1], world)
+            lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+            shard = period_slice(inst, lo, hi)
+            rows = [(t * mb + lo, t * mb + hi) for t in range(T)]
+        else:
+            inst = generate("medium", m=900, N=300, k=(20, 80))
+            if variant == "bundles":
+                inst = with_bundles(inst, L=90, seed=4)
+            bounds = partition(inst.seg_ptr, world)
+            lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+            shard = inst.segment_slice(lo, hi)
+            rows = [(lo, hi)]
 
-        # global column counts -> tau_j (what spfom_create does with an NCCL allreduce)
+        # global column counts -> tau (what spfom_create does with an NCCL allreduce)
         cnt = torch.from_numpy(np.bincount(shard.prod_idx, minlength=inst.N).astype(np.int64))
         dist.all_reduce(cnt)
         n = cnt.numpy()
         assert np.array_equal(n, np.bincount(inst.prod_idx, minlength=inst.N))
-        tau = np.where(n > 0, 0.9 / np.maximum(n, 1), 0.9)
+        if variant == "bundles":      # per resource: n_l = sum_{j uses l} n_j (reading c17)
+            nl = np.zeros(inst.num_resources, dtype=np.int64)
+            for j in range(inst.N):
+                nl[inst.bundle_res[inst.bundle_ptr[j]:inst.bundle_ptr[j + 1]]] += n[j]
+            tau = np.where(nl > 0, 0.9 / np.maximum(nl, 1), 0.9)
+        else:
+            tau = np.where(n > 0, 0.9 / np.maximum(n, 1), 0.9)
 
         S = oracle.OracleSolver(shard)
         S.tau_j[:] = tau
         ref = oracle.OracleSolver(inst)
-        a, b = int(inst.seg_ptr[lo]), int(inst.seg_ptr[hi])
+        ent = np.concatenate([np.arange(inst.seg_ptr[a], inst.seg_ptr[b]) for a, b in rows])
+        seg = np.concatenate([np.arange(a, b) for a, b in rows])
         for _t in range(40):
             s = torch.from_numpy(S.primal_shard())
             dist.all_reduce(s)
@@ -58,8 +77,8 @@ def _worker(rank, world, port, errq):
             ref.step()
             scale = max(float(np.abs(ref.eta).max()), 1e-300)
             assert np.abs(S.eta - ref.eta).max() <= 1e-12 * max(scale, 1.0), "eta drifted from single-rank run"
-            assert np.abs(S.y - ref.y[a:b]).max() <= 1e-12 * max(1.0, np.abs(ref.y).max())
-            assert np.abs(S.y0 - ref.y0[lo:hi]).max() <= 1e-12 * float(inst.arrival.max())
+            assert np.abs(S.y - ref.y[ent]).max() <= 1e-12 * max(1.0, np.abs(ref.y).max())
+            assert np.abs(S.y0 - ref.y0[seg]).max() <= 1e-12 * float(inst.arrival.max())
         # every rank holds bitwise-identical duals
         mine = torch.from_numpy(S.eta.copy())
         gathered = [torch.zeros_like(mine) for _ in range(world)]
@@ -73,11 +92,12 @@ def _worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_iteration_matches_single_rank(world):
+@pytest.mark.parametrize("world,variant", [(2, "plain"), (3, "plain"), (2, "bundles"), (3, "multi")])
+def test_sharded_iteration_matches_single_rank(world, variant):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
-    mp.start_processes(_worker, args=(world, _free_port(), errq), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), errq, variant), nprocs=world, join=True,
+                       start_method="spawn")
     assert errq.empty(), errq.get()
 
 

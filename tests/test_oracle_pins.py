@@ -499,3 +499,12 @@ def test_bundle_infinite_capacity_keeps_resource_duals_zero():
     for _ in range(20):
         S.step()
     assert np.all(S.eta == 0.0)
+
+
+# ------------------------------------------------------------ bid-price simulation helpers
+def test_sales_entropy_examples():
+    from paper_2602_22421_b200.sim import sales_entropy
+    assert abs(sales_entropy(np.array([3, 3, 3, 3])) - 2.0) <= 1e-15
+    assert sales_entropy(np.array([0, 7, 0])) == 0.0
+    assert abs(sales_entropy(np.array([2, 1, 1])) - 1.5) <= 1e-15
+    assert sales_entropy(np.zeros(5)) == 0.0
