@@ -409,3 +409,38 @@ def test_bundle_identity_incidence_equals_plain_path():
     assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
     a.close()
     b.close()
+
+
+# ------------------------------------------------------------ feature combinations
+@pytest.mark.parametrize("combo", ["paper-multi", "paper-bundles", "averaging-bundles", "averaging-multi",
+                                   "ragged-graph", "paper-medium-graph"])
+def test_feature_combinations_lockstep(combo):
+    """The layouts x presets the kernels branch on: exact argmax through the
+    shared-period kernel and with bundle prices, averaging with resource duals
+    and with [T][m] segment state, the ragged-bin instance and the paper preset
+    through the per-iteration graph instead of the persistent small kernel."""
+    from paper_2602_22421_b200 import Params
+    from spfom_inputs import with_bundles
+    if combo == "paper-multi":
+        inst, p, iters = generate("multi", m=300, N=200, k=(5, 60), T=3), Params.paper(mu=0.3), 60
+    elif combo == "paper-bundles":
+        inst = with_bundles(generate("small", m=400, N=150, k=(5, 40)), L=50, seed=6)
+        p, iters = Params.paper(mu=0.3), 60
+    elif combo == "averaging-bundles":
+        inst = with_bundles(generate("small", m=400, N=150, k=(5, 40)), L=50, seed=7)
+        p, iters = _params(averaging=True), 40
+    elif combo == "averaging-multi":
+        inst, p, iters = generate("multi", m=300, N=200, k=(5, 60), T=2), _params(averaging=True), 40
+    elif combo == "ragged-graph":
+        ks = [0, 1, 3, 16, 17, 33, 64, 65, 129, 257, 513, 1000, 50] * 4
+        inst, p, iters = _ragged_instance(ks, N=1100, seed=2), _params(exec_mode=1), 40
+    else:
+        inst, p, iters = generate("medium", m=1500, N=1000, k=(20, 200)), Params.paper(mu=0.0, exec_mode=1), 60
+    worst, gpu, cpu = lockstep(inst, p, iters)
+    if p.averaging:
+        yb, y0b, eb = gpu.averages()
+        lam, rmax = float(inst.arrival.max()), float(inst.price.max())
+        assert rel_inf(yb, cpu.ybar, lam) <= TOL_ITER and rel_inf(y0b, cpu.y0bar, lam) <= TOL_ITER
+        assert rel_inf(eb, cpu.etabar, rmax) <= TOL_ITER
+    gpu.close()
+    _assert_ok(worst)
