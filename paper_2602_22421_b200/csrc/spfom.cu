@@ -9,12 +9,14 @@
 // the usage accumulator -> K3 [-> averaging] -> tick).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <time.h>
 #include <omp.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -185,7 +187,7 @@ struct spfom_handle {
     int64_t L = 0;                                                  // resources (bundles / NRM), 0 = none
     std::vector<int32_t> bptr_h, bres_h;                            // relabelled bundle CSR (set_state)
     std::vector<int32_t> new2old, old2new;     // products
-    std::vector<int64_t> pos_map;              // original entry -> padded entry
+    std::unique_ptr<int64_t[]> pos_map;        // original entry -> padded entry [nnz] (no zero-fill)
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
@@ -544,7 +546,7 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
     char buf[256];
     const int64_t m = in->num_segments, N = in->num_products;
     if (m < 0 || N < 1 || in->nnz < 0 || !in->seg_ptr || (in->nnz > 0 && (!in->prod_idx || !in->attract)) ||
-        (m > 0 && (!in->no_purchase || !in->arrival)) || !in->price || !in->capacity)
+        (m > 0 && (!in->no_purchase || !in->arrival)) || !in->price || (in->num_resources <= 0 && !in->capacity))
         return fail(nullptr, SPFOM_EINVAL, "instance: missing array or bad size");
     if (in->seg_ptr[0] != 0 || in->seg_ptr[m] != in->nnz)
         return fail(nullptr, SPFOM_EDATA, "instance: seg_ptr[0] must be 0 and seg_ptr[m] == nnz");
@@ -552,7 +554,23 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
     const int64_t T = std::max<int64_t>(1, in->num_periods);
     if (T > 1 && p && p->blocks) return fail(nullptr, SPFOM_EINVAL, "sampled blocks are not supported with num_periods > 1");
     if (N >= INT32_MAX) return fail(nullptr, SPFOM_EDATA, "instance: num_products too large");
+    // per-segment rules: a parallel scan finds the first offending segment, the
+    // serial loop below (from there) reports it
+    int64_t first_bad = m;
+#pragma omp parallel for schedule(static, 4096) reduction(min : first_bad)
     for (int64_t i = 0; i < m; ++i) {
+        const int64_t a = in->seg_ptr[i], b = in->seg_ptr[i + 1];
+        bool ok = b >= a && !(T > 1 && (b - a + 3) / 4 > 128) && (b - a + 3) / 4 <= kMaxQuads &&
+                  in->no_purchase[i] > 0.0 && std::isfinite(in->no_purchase[i]);
+        for (int64_t t = 0; t < T && ok; ++t) ok = in->arrival[t * m + i] > 0.0 && std::isfinite(in->arrival[t * m + i]);
+        for (int64_t e = a; e < b && ok; ++e) {
+            const int32_t j = in->prod_idx[e];
+            const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
+            ok = j >= 0 && j < N && !(e > a && j <= in->prod_idx[e - 1]) && v > 0.0 && std::isfinite(v) && w >= 0.0 && w < v;
+        }
+        if (!ok && i < first_bad) first_bad = i;
+    }
+    for (int64_t i = first_bad; i < m; ++i) {
         const int64_t a = in->seg_ptr[i], b = in->seg_ptr[i + 1];
         if (b < a) { snprintf(buf, sizeof buf, "seg_ptr not monotone at segment %lld", (long long)i); return fail(nullptr, SPFOM_EDATA, buf); }
         if (T > 1 && (b - a + 3) / 4 > 128) {
@@ -622,11 +640,30 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
     return SPFOM_OK;
 }
 
+// SPFOM_TRACE_CREATE=1: host-side phase times of spfom_create on stderr
+struct PhaseTimer {
+    bool on = getenv("SPFOM_TRACE_CREATE") != nullptr;
+    double t0 = now();
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec + 1e-9 * ts.tv_nsec;
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        const double t = now();
+        fprintf(stderr, "[spfom_create] %-28s %8.1f ms\n", what, (t - t0) * 1e3);
+        t0 = t;
+    }
+};
+
 spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const spfom_dist *dist,
                           void *cuda_stream, void *workspace, size_t ws_bytes, spfom_handle **out) {
     if (!in || !out) return fail(nullptr, SPFOM_EINVAL, "spfom_create: NULL argument");
     *out = nullptr;
+    PhaseTimer ptimer;
     spfom_status st = validate(in, p);
+    ptimer.mark("validate");
     if (st != SPFOM_OK) return st;
     Plan pl;
     make_plan(in, p, pl);
@@ -679,6 +716,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     }
     const int64_t m = h->m, N = h->N;
 
+    ptimer.mark("plan+handle+streams");
     // ---- global column counts n_j
     std::vector<int64_t> counts(N + 1, 0);
     for (int64_t e = 0; e < in->nnz; ++e) counts[in->prod_idx[e]] += h->T;   // stacked segments (T per base row)
@@ -689,6 +727,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         if (cudaMemcpyAsync(counts.data(), dcounts, N * 8, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
             cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "D2H counts"; return bail(SPFOM_ECUDA); }
     }
+    ptimer.mark("column counts");
     // ---- popularity relabelling: new id = rank by (-n_j, j)
     h->new2old.resize(N);
     std::iota(h->new2old.begin(), h->new2old.end(), 0);
@@ -698,6 +737,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     h->n_present = 0;
     for (int64_t j = 0; j < N; ++j) h->n_present += counts[j] > 0;
 
+    ptimer.mark("relabelling");
     // ---- per-product arrays (relabelled), slot N = dummy
     const int64_t L = in->num_resources;
     h->L = L;
@@ -741,6 +781,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
     }
 
+    ptimer.mark("product arrays + bundles");
     // ---- length bins; device segment order = (bin, local id), so that every
     // bin is one contiguous range
     std::vector<int> segbin(std::max<int64_t>(m, 1));
@@ -762,6 +803,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
     }
 
+    ptimer.mark("bins + device order");
     // ---- padded quad CSR in device order
     std::vector<int32_t> qoff(m + 1, 0);
     for (int64_t k = 0; k < m; ++k) {
@@ -769,21 +811,31 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         qoff[k + 1] = qoff[k] + (int32_t)((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
     }
     const int64_t nq = qoff[m];
-    std::vector<int32_t> pidx(4 * std::max<int64_t>(nq, 1), (int32_t)N);
-    std::vector<double> vv(4 * std::max<int64_t>(nq, 1), 0.0), om(4 * std::max<int64_t>(nq, 1), 0.0);
+    // uninitialised host staging (the parallel loop writes every padded slot, pads included)
+    std::unique_ptr<int32_t[]> pidx(new int32_t[4 * std::max<int64_t>(nq, 1)]);
+    std::unique_ptr<double[]> vv(new double[4 * std::max<int64_t>(nq, 1)]), om(new double[4 * std::max<int64_t>(nq, 1)]);
     const int64_t T = h->T;
     std::vector<double2> segc(std::max<int64_t>(T * m, 1));
     std::vector<double4> segv(std::max<int64_t>(T * m, 1));
-    h->pos_map.assign(in->nnz, 0);
+    h->pos_map.reset(new int64_t[std::max<int64_t>(in->nnz, 1)]);
     h->seg_off.assign(in->seg_ptr, in->seg_ptr + m + 1);
     bool bad_numeric = false;
-#pragma omp parallel for schedule(dynamic, 4096)
+#pragma omp parallel
+    {
+    std::vector<std::pair<int32_t, int64_t>> order;                 // per-thread sort buffer
+#pragma omp for schedule(dynamic, 4096)
     for (int64_t k = 0; k < m; ++k) {
         const int64_t i = h->sorder[k];
         const int64_t a = in->seg_ptr[i], len = in->seg_ptr[i + 1] - a;
-        std::vector<std::pair<int32_t, int64_t>> order(len);
+        order.resize(len);
         for (int64_t q = 0; q < len; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
         std::sort(order.begin(), order.end());
+        const int64_t pend = 4 * (int64_t)qoff[k + 1];
+        for (int64_t p = 4 * (int64_t)qoff[k] + len; p < pend; ++p) {   // inert pads
+            pidx[p] = (int32_t)N;
+            vv[p] = 0.0;
+            om[p] = 0.0;
+        }
         double vt0 = in->no_purchase[i], svt = 0.0;
         const int64_t base = 4 * (int64_t)qoff[k];
         for (int64_t q = 0; q < len; ++q) {
@@ -804,8 +856,11 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
         if (!std::isfinite(vt0)) bad_numeric = true;
     }
+    }
+    if (nq == 0) { pidx[0] = (int32_t)N; vv[0] = 0.0; om[0] = 0.0; }
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
 
+    ptimer.mark("padded CSR (omp)");
     // ---- sampled block tables: per (iteration, bin) lists of device slots
     if (pl.sampled) {
         std::vector<int32_t> rowoff, blkids;
@@ -840,13 +895,14 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "sync"; return bail(SPFOM_ECUDA); }
     }
 
+    ptimer.mark("block tables");
     // ---- copies into the workspace
     auto H2D = [&](int slot, const void *src, size_t bytes) {
         return bytes == 0 || cudaMemcpyAsync(h->ws + h->pl.off[slot], src, bytes, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
     };
     std::vector<double> y0(std::max<int64_t>(T * m, 1));
     for (int64_t k = 0; k < T * m; ++k) y0[k] = segv[k].x;
-    bool ok = H2D(O_PIDX, pidx.data(), nq * 16) && H2D(O_V, vv.data(), nq * 32) && H2D(O_OM, om.data(), nq * 32) &&
+    bool ok = H2D(O_PIDX, pidx.get(), nq * 16) && H2D(O_V, vv.get(), nq * 32) && H2D(O_OM, om.get(), nq * 32) &&
               H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
               H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), D1 * 8) &&
               H2D(O_TAU, tau.data(), D1 * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
@@ -961,6 +1017,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             if (!okc) { h->err = "side stream creation failed"; return bail(SPFOM_ECUDA); }
         }
     }
+    ptimer.mark("H2D + state + modes");
     st = build_graph(h, false, &h->graph);
     if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
     if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_rest, 2);
@@ -970,6 +1027,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         if (st == SPFOM_OK) st = build_graph(h, true, &h->graph_rest_refresh, 2);
         if (st != SPFOM_OK) return bail(st);
     }
+    ptimer.mark("graphs");
     *out = h;
     return SPFOM_OK;
 }
@@ -1077,14 +1135,20 @@ spfom_status spfom_usage(spfom_handle *h, double *s) {
 static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, size_t pitch0, double *y,
                                  double *y0) {
     const int64_t T = h->T;
-    std::vector<double> tmp(4 * std::max<int64_t>(T * h->nq, 1)), t0(std::max<int64_t>(T * h->m, 1));
-    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), dy, T * h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
+    std::unique_ptr<double[]> tmp(new double[4 * std::max<int64_t>(T * h->nq, 1)]);   // no zero-fill
+    std::vector<double> t0(std::max<int64_t>(T * h->m, 1));
+    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.get(), dy, T * h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
     if (y0 && h->m)
         CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, T * h->m, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     for (int64_t t = 0; t < T; ++t) {
-        if (y)
-            for (int64_t e = 0; e < h->nnz; ++e) y[t * h->nnz + e] = tmp[4 * t * h->nq + h->pos_map[e]];
+        if (y) {
+            const int64_t *pm = h->pos_map.get();
+            const double *src = tmp.get() + 4 * t * h->nq;
+            double *dst = y + t * h->nnz;
+#pragma omp parallel for schedule(static)
+            for (int64_t e = 0; e < h->nnz; ++e) dst[e] = src[pm[e]];
+        }
         if (y0)
             for (int64_t k = 0; k < h->m; ++k) y0[t * h->m + h->sorder[k]] = t0[t * h->m + k];
     }
