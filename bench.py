@@ -407,7 +407,9 @@ def main():
                                         f"20 B/base nnz x {shard.nnz // T} + 16 B/nnz x {shard.nnz} + "
                                         f"4 B/base segment x {shard.m // T} + 32 B/segment x {shard.m} (T = {T} shared)"),
                          "k1_ms_avg": k1_ms, "rest_ms_avg": rest_ms, "k1_share_of_step": k1_ms / (ms / args.steps),
-                         "k1_timing": "CUDA events on the solver stream around the primal graph of every timed iteration",
+                         "k1_timing": ("CUDA events on the solver stream around the primal graph of every timed iteration"
+                                       if not info.get("persistent") else
+                                       "persistent small-regime kernel (whole iterations): CUDA events around all of them"),
                          "peak_source": peak_src, "frac_of_8tbs": k1_achieved / 8000.0},
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,

@@ -266,6 +266,8 @@ spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha);
  * handle's stream before and after the primal graph -- then synchronise and
  * write ms[0] = summed event time of the primal kernels over the k iterations,
  * ms[1] = event time from the first to the last event (all k iterations).
+ * In the small regime (spfom_info.persistent) the iterations run inside the
+ * persistent kernel: ms[0] = ms[1] = their event time.
  * Collective when world > 1.  Advances the iterate by k. */
 spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms);
 

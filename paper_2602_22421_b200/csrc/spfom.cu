@@ -1361,6 +1361,25 @@ spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms) {
 
 spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
     if (!h || !ms || k < 1) return SPFOM_EINVAL;
+    if (h->small) {
+        // the persistent small-regime kernel runs whole iterations: one event pair
+        // around all of them; the primal share is not separable (ms[0] = ms[1])
+        cudaEvent_t e0, e1;
+        CUDA_TRY(h, cudaEventCreate(&e0));
+        CUDA_TRY(h, cudaEventCreate(&e1));
+        CUDA_TRY(h, cudaEventRecord(e0, h->stream));
+        spfom_status st = step_small(h, k);
+        if (st == SPFOM_OK) {
+            CUDA_TRY(h, cudaEventRecord(e1, h->stream));
+            CUDA_TRY(h, cudaEventSynchronize(e1));
+            float t = 0.f;
+            CUDA_TRY(h, cudaEventElapsedTime(&t, e0, e1));
+            ms[0] = ms[1] = t;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return st;
+    }
     std::vector<cudaEvent_t> ev(2 * k + 1);
     for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
     spfom_status st = SPFOM_OK;
