@@ -143,13 +143,6 @@ __device__ __forceinline__ void st256_stream(double *p, double a, double b, doub
 #endif
 }
 
-// TMA bulk prefetch of a contiguous range into L2 (bytes: multiple of 16, 16-B aligned)
-__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const void *p) {
-    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
-}
 // shared-memory fp64 access through a 32-bit shared-window address (keeps
 // ptxas from rebuilding the generic->shared conversion in predicated code)
 __device__ __forceinline__ double lds_f64(uint32_t a) {
@@ -170,9 +163,6 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double x) {
 __device__ __forceinline__ void red_add_if(double *p, double v, bool pred) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p red.global.add.f64 [%0], %1;\n\t}"
                  :: "l"(p), "d"(v), "r"((int)pred) : "memory");
-}
-__device__ __forceinline__ void st_v2f64(double *p, double a, double b) {
-    asm volatile("st.global.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(a), "d"(b) : "memory");
 }
 __device__ __forceinline__ int idx_of(const int4 &q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
@@ -204,20 +194,6 @@ struct SegList {
     int32_t head;                // K1: products [0, head) privatised in shared memory (0 = none)
 };
 
-__device__ __forceinline__ bool seg_slot(const SegList &L, const DevState &S, int64_t slot, int64_t &i) {
-    if (L.row_off) {
-        const int64_t row = (*S.t) % L.block_iters;
-        const int32_t *ro = L.row_off + row * (L.nbins + 1);
-        const int64_t a = ro[L.bin], b = ro[L.bin + 1];
-        if (slot >= b - a) return false;
-        i = L.ids[a + slot];
-        return true;
-    }
-    if (slot >= L.count) return false;
-    i = L.ids ? (int64_t)L.ids[L.first + slot] : L.first + slot;
-    return true;
-}
-
 // The launch's segment list resolved once: ids (null = contiguous from first) and count.
 struct SegSpan {
     const int32_t *ids;
@@ -237,14 +213,4 @@ __device__ __forceinline__ bool span_slot(const SegSpan &P, int64_t slot, int64_
     i = P.ids ? (int64_t)P.ids[slot] : P.first + slot;
     return true;
 }
-
-__device__ __forceinline__ int64_t seg_count(const SegList &L, const DevState &S) {
-    if (L.row_off) {
-        const int64_t row = (*S.t) % L.block_iters;
-        const int32_t *ro = L.row_off + row * (L.nbins + 1);
-        return ro[L.bin + 1] - ro[L.bin];
-    }
-    return L.count;
-}
-
 }  // namespace spfom

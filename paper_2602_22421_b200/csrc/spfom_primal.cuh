@@ -345,9 +345,6 @@ __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 
 // ============================================================== k_primal_stream
 // Full sweep over segments [first, first + count) of one bin (contiguous).
-#ifndef SPFOM_WARP_HIST
-#define SPFOM_WARP_HIST 0
-#endif
 #ifndef SPFOM_SPREAD_C
 #define SPFOM_SPREAD_C 8
 #endif
@@ -377,8 +374,8 @@ struct StreamLayout {
     static constexpr uint32_t OFF_Y = OFF_OM + 32u * (QMAX + 1);           // double4 x (QMAX + 1)
     static constexpr uint32_t OFF_IDS = OFF_Y + 32u * (QMAX + 1);          // int4 x (QMAX + 1)
     static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
-    // head products per histogram: one per group (GPW of them) or one per warp
-    static constexpr int NHIST = SPFOM_WARP_HIST ? 1 : GPW;
+    // one head histogram per group (ids are distinct within a segment: no atomics)
+    static constexpr int NHIST = GPW;
     static constexpr int HH = SPFOM_HIST_TOTAL / NHIST;
     static constexpr uint32_t HIST = (uint32_t)NHIST * hist_stride(HH) * 8u;   // bytes per warp
     static constexpr uint32_t PER_WARP = SLOT + ((HIST + 127u) & ~127u);
@@ -418,8 +415,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
     double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + warp;
     double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q>());
-    double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) +
-                 (LY::NHIST > 1 ? gidx * HS : 0);
+    double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) + gidx * HS;
     const uint32_t ghead_s = smem_u32(ghead), hg_s = smem_u32(hg);
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
@@ -558,26 +554,12 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
         // a5: head -> histogram, warm head -> spread copies, tail -> s
-        if constexpr (LY::NHIST > 1) {
 #pragma unroll
-            for (int e = 0; e < NE; ++e) {
-                const int j = idx[e];
-                if (j < HH) {
-                    const uint32_t a = hg_s + 8u * (uint32_t)j;
-                    sts_f64(a, lds_f64_v(a) + yv[e]);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int gg = 0; gg < GPW; ++gg) {
-                if (gidx == gg) {
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) {
-                        const int j = idx[e];
-                        if (j < HH) hg[j] += yv[e];
-                    }
-                }
-                __syncwarp();
+        for (int e = 0; e < NE; ++e) {
+            const int j = idx[e];
+            if (j < HH) {
+                const uint32_t a = hg_s + 8u * (uint32_t)j;
+                sts_f64(a, lds_f64_v(a) + yv[e]);
             }
         }
 #pragma unroll
