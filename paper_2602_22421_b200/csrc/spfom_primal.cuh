@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
         }
     };
 
+
     ProjStats st;
     int32_t qc = 0;
     if (r0 < r1) {
@@ -526,8 +527,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
             om[4 * t + 0] = w01.x; om[4 * t + 1] = w01.y; om[4 * t + 2] = w23.x; om[4 * t + 3] = w23.y;
             z[4 * t + 0] = y01.x; z[4 * t + 1] = y01.y; z[4 * t + 2] = y23.x; z[4 * t + 3] = y23.y;
         }
-        // the slot is free: fetch round r + 1 into it while this round computes
-        fence_proxy_async_smem();
+        // the slot is free: fetch round r + 1 into it while this round computes.
+        // The warp barrier orders every lane's slot reads before the copy is
+        // issued (the consumer-release pattern of TMA pipelines); a
+        // fence.proxy.async here compiles to MEMBAR.ALL.CTA, which would also
+        // wait for the previous round's global reductions to drain.
         __syncwarp();
         if (r + 1 < r1) issue(r + 1, qn);
 
@@ -554,13 +558,15 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q>::WARPS, 1) k_primal_st
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
         // a5: head -> histogram, warm head -> spread copies, tail -> s
+        // ids are distinct within a segment and every group has its own
+        // histogram: all loads first, then all stores (no serial RMW chain)
+        {
+            double hv[NE];
 #pragma unroll
-        for (int e = 0; e < NE; ++e) {
-            const int j = idx[e];
-            if (j < HH) {
-                const uint32_t a = hg_s + 8u * (uint32_t)j;
-                sts_f64(a, lds_f64_v(a) + yv[e]);
-            }
+            for (int e = 0; e < NE; ++e) hv[e] = idx[e] < HH ? lds_f64_v(hg_s + 8u * (uint32_t)idx[e]) : 0.0;
+#pragma unroll
+            for (int e = 0; e < NE; ++e)
+                if (idx[e] < HH) sts_f64(hg_s + 8u * (uint32_t)idx[e], hv[e] + yv[e]);
         }
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
@@ -757,8 +763,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
                 v[4 * tq + 0] = v01.x; v[4 * tq + 1] = v01.y; v[4 * tq + 2] = v23.x; v[4 * tq + 3] = v23.y;
                 om[4 * tq + 0] = w01.x; om[4 * tq + 1] = w01.y; om[4 * tq + 2] = w23.x; om[4 * tq + 3] = w23.y;
             }
-            fence_proxy_async_smem();
-            __syncwarp();
+            __syncwarp();                                  // slot reads before the copy (see k_primal_stream)
             if ((r + 1) * T < u1) issueS(r + 1, qn, (r + 2) * T < u1);
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
@@ -792,7 +797,6 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
             const double2 y01 = yp[0], y23 = yp[1];
             z[4 * tq + 0] = y01.x; z[4 * tq + 1] = y01.y; z[4 * tq + 2] = y23.x; z[4 * tq + 3] = y23.y;
         }
-        fence_proxy_async_smem();
         __syncwarp();
         if (u + 1 < u1) {
             const int64_t rn = (u + 1) / T;
@@ -818,7 +822,13 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
 #pragma unroll
-        for (int e = 0; e < NE; ++e) sts_f64(ys_s + 256u * e, lds_f64_v(ys_s + 256u * e) + yv[e]);
+        {
+            double hv[NE];                                 // loads first: no serial RMW chain
+#pragma unroll
+            for (int e = 0; e < NE; ++e) hv[e] = lds_f64_v(ys_s + 256u * e);
+#pragma unroll
+            for (int e = 0; e < NE; ++e) sts_f64(ys_s + 256u * e, hv[e] + yv[e]);
+        }
 
         // ---- end of this warp's part of round r: a5 scatter of sum_t y
         if (u + 1 == u1 || (u + 1) / T != r) {
