@@ -41,8 +41,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-iters", type=int, default=50, help="unused (kept for old command lines)")
     ap.add_argument("--cache", default=None, help="directory to cache the generated instance (npz)")
-    ap.add_argument("--mode", default="throughput", choices=["throughput", "ttg"],
-                    help="ttg: time-to-gap of the full sweep vs sampled blocks B = m/2^k (SURVEY 8(f) rank 1)")
+    ap.add_argument("--mode", default="throughput", choices=["throughput", "ttg", "features"],
+                    help="ttg: time-to-gap of the full sweep vs sampled blocks B = m/2^k (SURVEY 8(f) rank 1); "
+                         "features: device throughput of the a8 / 8(f) rows (averaging, paper preset full and "
+                         "sampled, bundles, recovery) on --config")
     ap.add_argument("--stacked", action="store_true",
                     help="multi-period configs: pass the stacked instance as one period (no shared structure)")
     return ap.parse_args()
@@ -263,11 +265,74 @@ def run_ttg(args):
           flush=True)
 
 
+# --------------------------------------------------------------------- feature rows
+def run_features(args):
+    """One JSON line per row: iterations/s (CUDA events over `steps` timed
+    iterations after `warmup`, step_timed) and K1's share, for the converge
+    preset with and without averaging (a8), the paper preset (theta = inf exact
+    argmax, tau 0.1) full sweep and with sampled blocks B = m/4 (8(f) 1), the
+    NRM bundle instance (8(f) 3); then the device time of the SBLP -> CBLP
+    recovery of the converged iterate (8(f) 2)."""
+    import torch
+
+    from paper_2602_22421_b200 import Params, Solver
+    from spfom_inputs import block_sequence, with_bundles
+
+    inst = load_instance(args.config, args.cache)
+    peak, peak_src = measured_peaks()
+    steps, warm = max(1, min(args.steps, 500)), max(3, args.warmup)
+    m = inst.m
+    rows = [("converge", inst, Params.converge()),
+            ("converge + averaging (a8)", inst, Params.converge(averaging=True)),
+            ("paper preset, full sweep (theta = inf)", inst, Params.paper()),
+            ("paper preset, sampled B = m/4 (8(f) 1)", inst, Params.paper(blocks=block_sequence(m, m // 4, 64, 5)))]
+    if int(inst.meta.get("T", 1)) > 1:
+        rows.pop()            # sampled blocks are rejected with shared periods (spfom.h)
+    t0 = time.perf_counter()
+    binst = with_bundles(inst, seed=3)
+    rows.append((f"bundles / NRM, L = {binst.num_resources} resources (8(f) 3)", binst, Params.converge()))
+    gen_s = time.perf_counter() - t0
+    for label, ins, prm in rows:
+        s = Solver(ins, prm)
+        s.step(warm)
+        torch.cuda.synchronize()
+        k1, tot = s.step_timed(steps)
+        line = {"mode": "features", "row": label, "config": workload_config(ins, 1),
+                "value": steps / (tot / 1e3), "unit": "iterations/s", "steps": steps, "warmup": warm,
+                "ms_per_step": tot / steps, "k1_ms_avg": k1 / steps, "k1_share": k1 / tot,
+                "exec": "persistent (k_small)" if s.info()["persistent"] else "graph",
+                "launches_per_iteration": int(s.info()["launches_per_iteration"])}
+        if "bundles" in label:
+            line["bundle_generation_s"] = gen_s
+        if label == "converge":
+            s.step(max(0, 1000 - warm - steps))
+            ms = s.recover_timed()
+            nnz, T = ins.nnz, int(ins.meta.get("T", 1))
+            # algorithmic bytes: per entry id 4 + v 8 + omega 8 + y 8 + original id 4 read, order 4 + alpha 8
+            # written; per segment qoff 4 + (lambda, vt0) 16 + y0 8 read, alpha_0 8 written
+            rb = 44 * nnz + 36 * ins.m
+            print(json.dumps({"mode": "features", "row": "SBLP -> CBLP recovery (8(f) 2)",
+                              "config": workload_config(ins, 1), "iteration": s.iteration,
+                              "value": ins.m / (ms / 1e3), "unit": "segments/s", "ms": ms,
+                              "roofline": {"bound": "hbm", "achieved": rb / (ms / 1e3) / 1e9, "peak": peak,
+                                           "unit": "GB/s", "frac": rb / (ms / 1e3) / 1e9 / peak,
+                                           "bytes": rb, "bytes_rule": "44 B/nnz + 36 B/segment",
+                                           "peak_source": peak_src},
+                              "note": "device time of every k_recover launch (CUDA events, no host copies); "
+                                      "rank-by-counting sort per segment, so ALU-heavy for long rows"}),
+                  flush=True)
+        s.close()
+        print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------- GPU arm
 def main():
     args = parse_args()
     if args.mode == "ttg":
         run_ttg(args)
+        return
+    if args.mode == "features":
+        run_features(args)
         return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))

@@ -260,6 +260,13 @@ spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms);
  * arrays).  Synchronous; SPFOM_ENUMERIC if projection failures were counted. */
 spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha);
 
+/* Measurement helper for the recovery kernel (bench.py --mode features): run
+ * the device part of spfom_recover -- every chunk of every period, the same
+ * launches -- into the workspace only (no host copies, results discarded),
+ * with CUDA events on the handle's stream around all launches; synchronises
+ * and writes ms[0] = elapsed milliseconds, ms[1] = number of launches. */
+spfom_status spfom_recover_timed(spfom_handle *h, double *ms);
+
 /* Timed stepping (bench.py's timed region): enqueue k iterations exactly like
  * spfom_step -- each iteration replays two CUDA graphs, the primal kernels
  * (a1-a5) and the rest (a6-a8 + tick), with a CUDA event recorded on the

@@ -20,6 +20,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "spfom.h"
@@ -1414,28 +1415,63 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
     return st;
 }
 
-spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
-    if (!h || !order || !alpha) return SPFOM_EINVAL;
+}   // extern "C" (templates below)
+
+// k_recover over device slots [a, b) of period t, with the row capacity of the
+// chunk's longest row (kmax entries)
+template <int KM>
+void launch_recover_km(spfom_handle *h, int64_t a, int64_t b, int64_t t) {
+    constexpr int W = recover_warps<KM>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RecoverSmem));
+        cudaFuncSetAttribute(k_recover<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RecoverSmem<KM>));
         attr = true;
     }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recover<KM>, 32 * W, sizeof(RecoverSmem<KM>));
+    const int64_t blocks = std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)h->sm_count * std::max(1, per_sm), (b - a + W - 1) / W));
+    k_recover<KM><<<(unsigned)blocks, 32 * W, sizeof(RecoverSmem<KM>), h->stream>>>(
+        h->S, a, b, t, slot_ptr<int32_t>(h, O_ORIG), slot_ptr<int32_t>(h, O_RECORD), slot_ptr<double>(h, O_RECALPHA));
+}
+void launch_recover(spfom_handle *h, int64_t a, int64_t b, int64_t t, int64_t kmax) {
+    if (kmax <= 64) launch_recover_km<64>(h, a, b, t);
+    else if (kmax <= 256) launch_recover_km<256>(h, a, b, t);
+    else launch_recover_km<kRecoverMaxK>(h, a, b, t);
+}
+// chunks of device slots whose outputs fit the workspace scratch (CH entries),
+// with the longest row of each
+std::vector<std::array<int64_t, 3>> recover_chunks(const std::vector<int32_t> &qoff, int64_t m, int64_t CH) {
+    std::vector<std::array<int64_t, 3>> out;
+    for (int64_t a = 0; a < m;) {
+        int64_t b = a + 1, kmax = 4 * (int64_t)(qoff[a + 1] - qoff[a]);
+        while (b < m && 4 * (int64_t)(qoff[b + 1] - qoff[a]) <= CH && (b + 1 - a) <= CH) {
+            kmax = std::max<int64_t>(kmax, 4 * (int64_t)(qoff[b + 1] - qoff[b]));
+            ++b;
+        }
+        out.push_back({a, b, kmax});
+        a = b;
+    }
+    return out;
+}
+
+extern "C" {
+
+spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
+    if (!h || !order || !alpha) return SPFOM_EINVAL;
     const int64_t CH = recover_chunk(h->nq), m = h->m;
     std::vector<int32_t> qoff(m + 1);
     CUDA_TRY(h, cudaMemcpyAsync(qoff.data(), h->S.qoff, (m + 1) * 4, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     int32_t *dord = slot_ptr<int32_t>(h, O_RECORD);
     double *dal = slot_ptr<double>(h, O_RECALPHA);
-    const int32_t *dorig = slot_ptr<int32_t>(h, O_ORIG);
     std::vector<int32_t> hord(CH);
     std::vector<double> hal(2 * CH);
+    const auto chunks = recover_chunks(qoff, m, CH);
     for (int64_t t = 0; t < h->T; ++t) {
-        for (int64_t a = 0; a < m;) {
-            int64_t b = a + 1;
-            while (b < m && 4 * (int64_t)(qoff[b + 1] - qoff[a]) <= CH && (b + 1 - a) <= CH) ++b;
-            const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(h->sm_count * 2, (b - a + kRecoverWarps - 1) / kRecoverWarps));
-            k_recover<<<(unsigned)blocks, 32 * kRecoverWarps, sizeof(RecoverSmem), h->stream>>>(h->S, a, b, t, dorig, dord, dal);
+        for (const auto &c : chunks) {
+            const int64_t a = c[0], b = c[1];
+            launch_recover(h, a, b, t, c[2]);
             CUDA_TRY(h, cudaGetLastError());
             const int64_t ne = 4 * (int64_t)(qoff[b] - qoff[a]);
             if (ne) CUDA_TRY(h, cudaMemcpyAsync(hord.data(), dord, ne * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1450,10 +1486,34 @@ spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
                 for (int64_t r = 0; r < len; ++r) o[r] = hord[ob + r];
                 for (int64_t l = 0; l <= len; ++l) al[l] = hal[ab + l];
             }
-            a = b;
         }
     }
     return check_counters(h);
+}
+
+spfom_status spfom_recover_timed(spfom_handle *h, double *ms) {
+    if (!h || !ms) return SPFOM_EINVAL;
+    const int64_t CH = recover_chunk(h->nq), m = h->m;
+    std::vector<int32_t> qoff(m + 1);
+    CUDA_TRY(h, cudaMemcpyAsync(qoff.data(), h->S.qoff, (m + 1) * 4, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    const auto chunks = recover_chunks(qoff, m, CH);   // the same launches as spfom_recover
+    cudaEvent_t e0, e1;
+    CUDA_TRY(h, cudaEventCreate(&e0));
+    CUDA_TRY(h, cudaEventCreate(&e1));
+    CUDA_TRY(h, cudaEventRecord(e0, h->stream));
+    for (int64_t t = 0; t < h->T; ++t)
+        for (const auto &c : chunks) launch_recover(h, c[0], c[1], t, c[2]);
+    CUDA_TRY(h, cudaGetLastError());
+    CUDA_TRY(h, cudaEventRecord(e1, h->stream));
+    CUDA_TRY(h, cudaEventSynchronize(e1));
+    float f = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ms[0] = f;
+    ms[1] = (double)(chunks.size() * h->T);
+    return SPFOM_OK;
 }
 
 int64_t spfom_iteration(const spfom_handle *h) { return h ? h->iter : -1; }

@@ -274,28 +274,35 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small(DevState S, SmallArg
 //   alpha_l = (u_(l) - u_(l+1)) D(S_l) / lambda,  u_(0) = U, u_(k+1) = 0,
 //   D(S) = vt0 + sum_{j in S} (v_j - w_j).
 // One warp per segment of the device-slot chunk [a, b); rank by counting
-// (k <= 1024), warp-scan of the sorted vt for D.  Outputs for slot k start at
-// 4 (qoff[k] - qoff[a]) (order, original ids) and that + (k - a) (alpha).
-constexpr int kRecoverWarps = 4;
+// (k <= KM, the capacity of the warp's shared-memory rows, chosen per chunk
+// from its longest row so that short rows keep many warps per SM), warp-scan
+// of the sorted vt for D.  Outputs for slot k start at 4 (qoff[k] - qoff[a])
+// (order, original ids) and that + (k - a) (alpha).
 constexpr int kRecoverMaxK = 1024;
+template <int KM>
+__host__ __device__ constexpr int recover_warps() { return KM > 256 ? 4 : 8; }
+template <int KM>
 struct RecoverSmem {
-    double u[kRecoverWarps][kRecoverMaxK];      // row order
-    double vt[kRecoverWarps][kRecoverMaxK];
-    double su[kRecoverWarps][kRecoverMaxK];     // sorted order
-    double svt[kRecoverWarps][kRecoverMaxK];
-    int32_t oid[kRecoverWarps][kRecoverMaxK];
+    static constexpr int W = recover_warps<KM>();
+    double u[W][KM];      // row order
+    double vt[W][KM];
+    double su[W][KM];     // sorted order
+    double svt[W][KM];
+    int32_t oid[W][KM];
 };
 
-__global__ void __launch_bounds__(32 * kRecoverWarps) k_recover(DevState S, int64_t a, int64_t b, int64_t t,
+template <int KM>
+__global__ void __launch_bounds__(32 * recover_warps<KM>()) k_recover(DevState S, int64_t a, int64_t b, int64_t t,
                                                                 const int32_t *orig_of, int32_t *order_out,
                                                                 double *alpha_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    RecoverSmem &sm = *reinterpret_cast<RecoverSmem *>(smem_raw);
+    RecoverSmem<KM> &sm = *reinterpret_cast<RecoverSmem<KM> *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *u = sm.u[warp], *vt = sm.vt[warp], *su = sm.su[warp], *svt = sm.svt[warp];
     int32_t *oid = sm.oid[warp];
     const int64_t qa = S.qoff[a];
-    for (int64_t k = a + (int64_t)blockIdx.x * kRecoverWarps + warp; k < b; k += (int64_t)gridDim.x * kRecoverWarps) {
+    constexpr int W = recover_warps<KM>();
+    for (int64_t k = a + (int64_t)blockIdx.x * W + warp; k < b; k += (int64_t)gridDim.x * W) {
         const int64_t q0 = S.qoff[k], q1 = S.qoff[k + 1];
         const double2 sc = S.segc[t * S.m + k];                // (lambda, vt0)
         const double y0 = S.segv[t * S.m + k].x;
@@ -326,9 +333,11 @@ __global__ void __launch_bounds__(32 * kRecoverWarps) k_recover(DevState S, int6
             const double ue = u[e];
             const int32_t ie = oid[e];
             int rank = 0;
+#pragma unroll 8
             for (int f = 0; f < kk; ++f) {
                 const double uf = u[f];
-                rank += (uf > ue || (uf == ue && oid[f] < ie)) ? 1 : 0;
+                rank += uf > ue ? 1 : 0;
+                if (uf == ue) rank += oid[f] < ie ? 1 : 0;   // ties (and f = e): rare, by id
             }
             su[rank] = ue;
             svt[rank] = vt[e];

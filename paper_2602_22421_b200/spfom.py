@@ -24,8 +24,9 @@ STATUS = {0: "SPFOM_OK", 1: "SPFOM_EINVAL", 2: "SPFOM_EDATA", 3: "SPFOM_ENUMERIC
 
 EXPORTED = ("spfom_workspace_bytes", "spfom_create", "spfom_step", "spfom_duals", "spfom_primal", "spfom_usage",
             "spfom_averages", "spfom_objective", "spfom_residuals", "spfom_set_state", "spfom_info",
-            "spfom_time_kernels", "spfom_step_timed", "spfom_recover", "spfom_iteration", "spfom_last_error", "spfom_destroy", "spfom_partition",
-            "spfom_nccl_unique_id", "spfom_build_info", "spfom_abi_sizes")
+            "spfom_time_kernels", "spfom_step_timed", "spfom_recover", "spfom_recover_timed", "spfom_iteration",
+            "spfom_last_error", "spfom_destroy", "spfom_partition", "spfom_nccl_unique_id", "spfom_build_info",
+            "spfom_abi_sizes")
 
 
 class SpfomError(RuntimeError):
@@ -117,6 +118,7 @@ def load_library() -> C.CDLL:
         L.spfom_time_kernels.argtypes = [vp, i64, vp]
         L.spfom_step_timed.argtypes = [vp, i64, vp]
         L.spfom_recover.argtypes = [vp, vp, vp]
+        L.spfom_recover_timed.argtypes = [vp, vp]
         L.spfom_iteration.argtypes = [vp]
         L.spfom_iteration.restype = i64
         L.spfom_last_error.argtypes = [vp]
@@ -322,6 +324,13 @@ class Solver:
         alpha = np.empty(self.nnz + self.m)
         _check(load_library().spfom_recover(self._h, order.ctypes.data, alpha.ctypes.data), self._h)
         return order, alpha
+
+    def recover_timed(self) -> float:
+        """Device milliseconds of the recovery kernels over the whole instance
+        (spfom_recover_timed: same launches as recover(), no host copies)."""
+        ms = np.zeros(2)
+        _check(load_library().spfom_recover_timed(self._h, ms.ctypes.data), self._h)
+        return float(ms[0])
 
     def step_timed(self, k: int):
         """k iterations (two graph replays each) with CUDA events around the
