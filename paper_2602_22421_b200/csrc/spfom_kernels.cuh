@@ -329,19 +329,37 @@ __global__ void __launch_bounds__(32 * recover_warps<KM>()) k_recover(DevState S
         __syncwarp();
         // rank by counting: u descending, ties by ascending original product id
         const int64_t ob = 4 * (q0 - qa), ab = ob + (k - a);
-        for (int e = lane; e < kk; e += 32) {
-            const double ue = u[e];
-            const int32_t ie = oid[e];
-            int rank = 0;
+        // each lane ranks NR of the row's entries (lane, lane + 32, ..) in one pass over u
+        constexpr int NR = KM <= 64 ? 2 : 1;
+        for (int e0 = lane; e0 < kk; e0 += 32 * NR) {
+            double ue[NR];
+            int32_t ie[NR];
+            int rank[NR];
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const int e = e0 + 32 * c;
+                ue[c] = e < kk ? u[e] : -1.0;          // u >= 0: an absent entry ranks last
+                ie[c] = e < kk ? oid[e] : INT32_MAX;
+                rank[c] = 0;
+            }
 #pragma unroll 8
             for (int f = 0; f < kk; ++f) {
                 const double uf = u[f];
-                rank += uf > ue ? 1 : 0;
-                if (uf == ue) rank += oid[f] < ie ? 1 : 0;   // ties (and f = e): rare, by id
+#pragma unroll
+                for (int c = 0; c < NR; ++c) {
+                    rank[c] += uf > ue[c] ? 1 : 0;
+                    if (uf == ue[c]) rank[c] += oid[f] < ie[c] ? 1 : 0;   // ties (and f = e): rare, by id
+                }
             }
-            su[rank] = ue;
-            svt[rank] = vt[e];
-            order_out[ob + rank] = ie;
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const int e = e0 + 32 * c;
+                if (e < kk) {
+                    su[rank[c]] = ue[c];
+                    svt[rank[c]] = vt[e];
+                    order_out[ob + rank[c]] = ie[c];
+                }
+            }
         }
         __syncwarp();
         // D_l = vt0 + sum_{r < l} vt_(r): each lane scans one contiguous chunk of l
