@@ -69,9 +69,15 @@ thread_local std::string g_create_error;
 #define SPFOM_BIN2_G 4   // 8 segments per warp: the per-warp Newton / reduction overhead is shared by more rows
 #define SPFOM_BIN2_Q 4
 #endif
-#define SPFOM_BINS(X) X(0, 4, 1) X(1, 4, 2) X(2, SPFOM_BIN2_G, SPFOM_BIN2_Q) X(3, 16, 2) X(4, 32, 2) X(5, 32, 4) X(6, 32, 8)
-struct BinCfg { int G, Q; };
-#define SPFOM_BIN_INIT(B, G, Q) {G, Q},
+// E > 0: rows of at most E quads; the full-sweep stream kernel uses the entry
+// mapping (4 lanes x E entries, StreamLayout), the other kernels the (G, Q) one.
+#ifndef SPFOM_BIN_E
+#define SPFOM_BIN_E 13   // k = 49..52 entries (the BASELINE k = 50 configs)
+#endif
+#define SPFOM_BINS(X) X(0, 4, 1, 0) X(1, 4, 2, 0) X(2, 4, 4, SPFOM_BIN_E) X(3, SPFOM_BIN2_G, SPFOM_BIN2_Q, 0) \
+    X(4, 16, 2, 0) X(5, 32, 2, 0) X(6, 32, 4, 0) X(7, 32, 8, 0)
+struct BinCfg { int G, Q, E; };
+#define SPFOM_BIN_INIT(B, G, Q, E) {G, Q, E},
 constexpr BinCfg kBins[] = {SPFOM_BINS(SPFOM_BIN_INIT)};
 #undef SPFOM_BIN_INIT
 constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
@@ -82,9 +88,11 @@ constexpr int wide_q(int G, int Q) { return G * Q / wide_g(G, Q); }
 
 constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
 
+constexpr int64_t bin_cap(const BinCfg &c) { return c.E > 0 ? c.E : (int64_t)c.G * c.Q; }   // quads
+
 int bin_of(int64_t nq) {
     for (int b = 0; b < kNumBins; ++b)
-        if (nq <= (int64_t)kBins[b].G * kBins[b].Q) return b;
+        if (nq <= bin_cap(kBins[b])) return b;
     return -1;
 }
 
@@ -255,24 +263,25 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
 
 // Full sweep of a contiguous bin: one persistent 12-warp block per SM; the
 // rest of the opt-in shared memory stages the head of g.
-template <int G, int Q, bool ARGMAX>
+template <int G, int Q, bool ARGMAX, int EQ = 0>
 void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
+    using LY = StreamLayout<G, Q, EQ>;
     static int hg_cap = -1;
-    constexpr size_t fixed = stream_smem_fixed<G, Q>();
+    constexpr size_t fixed = stream_smem_fixed<G, Q, EQ>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
-        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(fixed + (size_t)hg_cap * 8));
     }
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
-    L.hh = (int32_t)std::min<int64_t>(StreamLayout<G, Q>::HH, S.N);
-    const int64_t rounds = (L.count + StreamLayout<G, Q>::GPW - 1) / StreamLayout<G, Q>::GPW;
-    constexpr int W = StreamLayout<G, Q>::WARPS;
+    L.hh = (int32_t)std::min<int64_t>(LY::HH, S.N);
+    const int64_t rounds = (L.count + LY::GPW - 1) / LY::GPW;
+    constexpr int W = LY::WARPS;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
-    k_primal_stream<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+    k_primal_stream<G, Q, ARGMAX, EQ><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
 // Multi-period shared structure: units = rounds x T over one persistent block per SM.
@@ -298,7 +307,7 @@ void launch_mp(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
 
 void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q)                                                                      \
+#define CASE(B, G, Q, E)                                                                   \
     case B:                                                                                \
         if constexpr (Q <= 4) {                                                            \
             if (argmax) launch_mp<G, Q, true>(S, L, sms, st);                              \
@@ -319,15 +328,15 @@ bool prefer_wide(int64_t count, int sms) {
 
 void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q)                                                                      \
+#define CASE(B, G, Q, E)                                                                   \
     case B:                                                                                \
         if constexpr (Q <= 4) {                                                            \
             constexpr int WG = wide_g(G, Q), WQ = wide_q(G, Q);                            \
             if (prefer_wide<G, Q>(L.count, sms) && (WG != G)) {                            \
                 if (argmax) launch_stream<WG, WQ, true>(S, L, sms, st);                    \
                 else launch_stream<WG, WQ, false>(S, L, sms, st);                          \
-            } else if (argmax) launch_stream<G, Q, true>(S, L, sms, st);                   \
-            else launch_stream<G, Q, false>(S, L, sms, st);                                \
+            } else if (argmax) launch_stream<G, Q, true, E>(S, L, sms, st);                \
+            else launch_stream<G, Q, false, E>(S, L, sms, st);                             \
         }                                                                                  \
         break;
         SPFOM_BINS(CASE)
@@ -340,7 +349,7 @@ void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L,
 void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const SegList &L, int64_t cnt, int sms,
                      cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q)                                                                      \
+#define CASE(B, G, Q, E)                                                                   \
     case B: {                                                                              \
         constexpr int WG = wide_g(G, Q), WQ = wide_q(G, Q);                                \
         if (argmax) {                                                                      \
@@ -360,7 +369,7 @@ void primal_dispatch(int b, bool argmax, bool sampled, const DevState &S, const 
 void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, int64_t seg_off, int64_t quad_off,
                     cudaStream_t st) {
     switch (b) {
-#define CASE(B, G, Q) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part, seg_off, quad_off); break;
+#define CASE(B, G, Q, E) case B: k_resid_seg<G, Q><<<kResidBlocks, kThreads, 0, st>>>(S, L, part, seg_off, quad_off); break;
         SPFOM_BINS(CASE)
 #undef CASE
     }
@@ -1002,7 +1011,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         int64_t wtot = 0, w[kNumBins] = {0};
         for (int b = 0; b < kNumBins; ++b) {
             const int64_t cnt = pl.sampled ? h->pl.bin_count[b] : (h->bin_first[b + 1] - h->bin_first[b]);
-            w[b] = pl.sampled ? cnt * (int64_t)kBins[b].G * kBins[b].Q
+            w[b] = pl.sampled ? cnt * bin_cap(kBins[b])
                               : (int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt;
             if (cnt > 0) h->nbins_active += 1;
             wtot += w[b];

@@ -105,6 +105,19 @@ def test_ragged_lengths_cross_every_bin_and_pad():
     _assert_ok(worst)
 
 
+@pytest.mark.parametrize("preset", ["converge", "paper"])
+def test_entry_mapped_bin_lockstep(preset):
+    """Rows of 49..52 entries (13 quads, the k = 50 configs) run on the full-
+    sweep stream kernel's entry mapping (bin E = 13: 4 lanes x 13 entries,
+    DESIGN.md §7).  24000 segments give every warp >= 2 rounds, so the
+    throughput mapping runs, not the wide latency one; pads of width 0..3."""
+    inst = generate("huge", m=24000, N=3000, k=(49, 52))
+    p = _params(exec_mode=1) if preset == "converge" else _paper(mu=0.5, exec_mode=1)
+    worst, gpu, _ = lockstep(inst, p, 30)
+    gpu.close()
+    _assert_ok(worst)
+
+
 def test_mnl_special_case_lockstep():
     """omega = 0 (MNL) is the GAM special case."""
     inst = generate("small", m=500, N=300, k=(10, 80))
