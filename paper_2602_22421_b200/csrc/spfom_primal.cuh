@@ -351,6 +351,9 @@ __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 #ifndef SPFOM_HIST_TOTAL
 #define SPFOM_HIST_TOTAL 1024      // head products privatised per warp (split over its groups)
 #endif
+#ifndef SPFOM_HIST_TOTAL_E
+#define SPFOM_HIST_TOTAL_E SPFOM_HIST_TOTAL   // entry-mapped layouts have a smaller slot: room for more
+#endif
 #ifndef SPFOM_STREAM_WARPS
 #define SPFOM_STREAM_WARPS 12        // 8 entries per lane: 168 registers -> 12 warps per SM
 #endif
@@ -385,7 +388,7 @@ struct StreamLayout {
     static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
     // one head histogram per group (ids are distinct within a segment: no atomics)
     static constexpr int NHIST = GPW;
-    static constexpr int HH = SPFOM_HIST_TOTAL / NHIST;
+    static constexpr int HH = (EQ ? SPFOM_HIST_TOTAL_E : SPFOM_HIST_TOTAL) / NHIST;
     static constexpr uint32_t HIST = (uint32_t)NHIST * hist_stride(HH) * 8u;   // bytes per warp
     static constexpr uint32_t PER_WARP = SLOT + ((HIST + 127u) & ~127u);
 };
