@@ -113,7 +113,7 @@ struct Plan {
 enum Slot {
     O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
     O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
-    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_NSLOTS
+    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_WORK, O_NSLOTS
 };
 
 constexpr int kSpreadCopies = SPFOM_SPREAD_C;
@@ -169,6 +169,7 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_RESPROD] = (size_t)kResidBlocks * 8 * 8;
     sz[O_COUNTERS] = 8 * 8;
     sz[O_T] = 8;
+    sz[O_WORK] = 8 * kNumBins;   // K1 stream: dynamic round-chunk counters, one per bin
     sz[O_COUNTS] = N1 * 8;
     // recovery scratch (spfom_recover works in chunks of at most recover_chunk() padded entries)
     sz[O_RECORD] = (size_t)recover_chunk(pl.nq) * 4;
@@ -406,12 +407,17 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 StreamList SL{};
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
+                SL.work = slot_ptr<unsigned long long>(h, O_WORK) + b;
                 // several bins: concurrent persistent kernels on disjoint SM shares
                 // (forked streams; inside a graph they become parallel branches)
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
                 cudaStream_t st = h->nbins_active > 1 ? h->side[b] : h->stream;
-                if (h->T > 1) mp_dispatch(b, argmax, S, SL, sms, st);
-                else stream_dispatch(b, argmax, S, SL, sms, st);
+                if (h->T > 1) {
+                    mp_dispatch(b, argmax, S, SL, sms, st);
+                } else {
+                    CUDA_TRY(h, cudaMemsetAsync(SL.work, 0, 8, st));   // dynamic round chunks start at 0
+                    stream_dispatch(b, argmax, S, SL, sms, st);
+                }
                 ++nl;
                 continue;
             }
@@ -925,7 +931,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
     ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, D1 * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
-         Z(O_COUNTERS, 64) && Z(O_T, 8);
+         Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 8 * kNumBins);
     if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, D1 * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
@@ -1547,3 +1553,12 @@ void spfom_destroy(spfom_handle *h) {
 }
 
 }  // extern "C"
+
+#ifdef SPFOM_DIAG_TIME
+extern "C" int spfom_diag_time(uint64_t *out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, spfom::g_diag_time, sizeof(uint64_t) * (size_t)n);
+}
+extern "C" int spfom_diag_loops(uint32_t *out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, spfom::g_diag_loops, sizeof(uint32_t) * (size_t)n);
+}
+#endif

@@ -137,6 +137,10 @@ __device__ __forceinline__ double y_entry(double z, double v, double om, double 
     return y;
 }
 
+#ifdef SPFOM_DIAG_TIME
+__device__ uint64_t g_diag_time[2 * 148 * 16];   // diagnostic: per-warp start / end of the last K1 launch
+__device__ uint32_t g_diag_loops[148 * 16];      // diagnostic: Newton loop trips per warp (cumulative)
+#endif
 struct ProjStats {
     unsigned long long passes = 0, failures = 0, restarts = 0;
 };
@@ -163,6 +167,9 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
     int passes = 0;
     const int restart_at = max_newton / 2;
     while (__any_sync(0xffffffffu, go)) {
+#ifdef SPFOM_DIAG_TIME
+        g_diag_loops[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] += ((threadIdx.x & 31) == 0);
+#endif
         // safeguard: a segment still unconverged after half the budget restarts
         // from the cold point (nu, kappa, U) = ((z0 + sum z - lam)/(k+1), 0, lam/(vt0 + sum vt))
         if (__any_sync(0xffffffffu, go && passes == restart_at)) {
@@ -271,7 +278,11 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
     if (active && (threadIdx.x & (G - 1)) == 0) {
         st.passes += (unsigned long long)passes;
         st.failures += failed ? 1ull : 0ull;
+#ifdef SPFOM_DIAG_LONG
+        st.restarts += (passes > SPFOM_DIAG_LONG) ? 1ull : 0ull;   // diagnostic: segments needing many passes
+#else
         st.restarts += restarted ? 1ull : 0ull;
+#endif
     }
 #pragma unroll
     for (int e = 0; e < NE; ++e) yv[e] = y_entry(z[e], v[e], om[e], x0, x1, x2);
@@ -351,6 +362,9 @@ __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 #ifndef SPFOM_HIST_TOTAL
 #define SPFOM_HIST_TOTAL 1024      // head products privatised per warp (split over its groups)
 #endif
+#ifndef SPFOM_DYN_CH
+#define SPFOM_DYN_CH 2   // rounds per dynamically claimed chunk (0: static contiguous partition per warp)
+#endif
 #ifndef SPFOM_HIST_TOTAL_E
 #define SPFOM_HIST_TOTAL_E SPFOM_HIST_TOTAL   // entry-mapped layouts have a smaller slot: room for more
 #endif
@@ -398,6 +412,7 @@ struct StreamList {
     int64_t first, count;   // segments [first, first + count), all of one bin
     int32_t ghead;          // g staged in shared memory for products [0, ghead)
     int32_t hh;             // group histograms cover products [0, hh) (<= Layout::HH)
+    unsigned long long *work;   // dynamic round chunks: counter zeroed before the launch
 };
 
 template <int G, int Q, int EQ = 0>
@@ -449,12 +464,47 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     }
     __syncthreads();
     (void)hist_all;
+#ifdef SPFOM_DIAG_TIME
+    uint64_t t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
-    // this warp's rounds [r0, r1) of GPW consecutive segments
-    const int64_t rounds = (L.count + GPW - 1) / GPW;
-    const int64_t W = (int64_t)gridDim.x * LY::WARPS;
-    const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
-    const int64_t r0 = rounds * gw / W, r1 = rounds * (gw + 1) / W;
+    // Rounds of GPW consecutive segments.  SPFOM_DYN_CH > 0: warps claim
+    // chunks of CH rounds from a global counter (the SMs of the two dies do
+    // not run at the same speed: a static split leaves one die idle at the
+    // end); the next chunk is claimed one chunk ahead, so the atomic's latency
+    // is hidden.  Rounds come from a 3-deep queue q0 (current), q1 (its TMA
+    // is issued during q0), q2 (q1's copy also fetches q2's offsets).
+    const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
+    constexpr int CH = SPFOM_DYN_CH;
+    const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
+    auto grab = [&]() -> int32_t {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(L.work, 1ull);
+        return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
+    };
+    int32_t fpos = 0, fend = 0, fpend = 0;
+    if constexpr (CH > 0) {
+        fpend = grab();
+    } else {
+        const int64_t W = (int64_t)gridDim.x * LY::WARPS;
+        const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
+        fpos = (int32_t)(rounds * gw / W);
+        fend = (int32_t)(rounds * (gw + 1) / W);
+    }
+    auto fnext = [&]() -> int32_t {
+        if constexpr (CH > 0) {
+            if (fpos >= fend) {
+                if (fpend >= nch) return -1;
+                fpos = fpend * CH;
+                fend = min(fpos + CH, rounds);
+                fpend = grab();
+            }
+        } else {
+            if (fpos >= fend) return -1;
+        }
+        return fpos++;
+    };
 
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
@@ -462,17 +512,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         k = k < L.count ? k : L.count;
         return S.qoff[L.first + k];
     };
-    // lanes 0..6 issue the bulk copies of round r (q: this lane's qoff of round r):
-    // segment state, quads, and (when the warp has a round r + 1) the 16-B
-    // aligned qoff window that holds round r + 1's offsets
-    auto issue = [&](int64_t r, int32_t q) {
+    // lane 0 issues the bulk copies of round r (q: this lane's qoff of round r):
+    // segment state, quads, and (rw >= 0) the 16-B aligned qoff window that
+    // holds round rw's offsets
+    auto issue = [&](int64_t r, int32_t q, int64_t rw) {
         const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
         const int64_t s0 = L.first + GPW * r;
         const int64_t left = L.count - GPW * r;
         const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
-        const int64_t w0 = (s0 + GPW) & ~(int64_t)3;                  // window of round r + 1
-        const uint32_t wbytes = (r + 1 < r1) ? 4u * LY::QW : 0u;
+        const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;        // window of round rw
+        const uint32_t wbytes = rw >= 0 ? 4u * LY::QW : 0u;
         // one elected lane, straight-line: the copies take uniform operands
         if (lane == 0) {
             mbar_arrive_expect_tx(bar, 48u * n + 112u * nq + wbytes);
@@ -492,17 +542,20 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 
     ProjStats st;
     int32_t qc = 0;
-    if (r0 < r1) {
-        qc = qload(r0);
-        issue(r0, qc);
+    int32_t q0 = fnext(), q1 = fnext(), q2 = fnext();
+    if (q0 >= 0) {
+        qc = qload(q0);
+        issue(q0, qc, q1);
     }
-    for (int64_t r = r0; r < r1; ++r) {
-        mbar_wait(bar, (uint32_t)((r - r0) & 1));
-        // round r + 1's offsets from the window that arrived with this round
+    uint32_t phase = 0;
+    for (; q0 >= 0; q0 = q1, q1 = q2, q2 = fnext(), phase ^= 1u) {
+        const int64_t r = q0;
+        mbar_wait(bar, phase);
+        // round q1's offsets from the window that arrived with this round
         int32_t qn = 0;
-        if (r + 1 < r1) {
-            const int64_t s1 = L.first + GPW * (r + 1);
-            int64_t k = GPW * (r + 1) + (lane < GPW ? lane : GPW);
+        if (q1 >= 0) {
+            const int64_t s1 = L.first + GPW * (int64_t)q1;
+            int64_t k = GPW * (int64_t)q1 + (lane < GPW ? lane : GPW);
             k = k < L.count ? k : L.count;
             qn = reinterpret_cast<const int32_t *>(slot + LY::OFF_QW)[L.first + k - (s1 & ~(int64_t)3)];
         }
@@ -557,7 +610,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         // fence.proxy.async here compiles to MEMBAR.ALL.CTA, which would also
         // wait for the previous round's global reductions to drain.
         __syncwarp();
-        if (r + 1 < r1) issue(r + 1, qn);
+        if (q1 >= 0) issue(q1, qn, q2);
 
         // a2: price gather (g[N] = 0 for pads; head from shared memory)
 #pragma unroll
@@ -607,6 +660,14 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         }
         qc = qn;
     }
+#ifdef SPFOM_DIAG_TIME
+    if (lane == 0) {
+        uint64_t t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        g_diag_time[2 * (blockIdx.x * LY::WARPS + warp)] = t_start;
+        g_diag_time[2 * (blockIdx.x * LY::WARPS + warp) + 1] = t_end;
+    }
+#endif
     if constexpr (!ARGMAX) {
         if (st.passes) {
             atomicAdd(S.counters + 1, st.passes);
