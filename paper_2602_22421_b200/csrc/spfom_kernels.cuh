@@ -38,14 +38,25 @@ __device__ __forceinline__ void tick_last_block(const DevState &S) {
 }
 
 // a7 for one product j (Eq. 17 with extrapolation and per-product tau_j)
+// fold of K1's spread copies of product j into acc, in fixed copy order
+// (deterministic); all copies are loaded before any is cleared, so the loads
+// are independent (one memory latency, not spread_c of them)
+__device__ __forceinline__ double fold_spread(const DevState &S, int64_t j, double acc) {
+    double part[SPFOM_SPREAD_C];
+#pragma unroll
+    for (int c = 0; c < SPFOM_SPREAD_C; ++c)
+        part[c] = c < S.spread_c ? S.spread[(size_t)c * S.spread_n + j] : 0.0;
+#pragma unroll
+    for (int c = 0; c < SPFOM_SPREAD_C; ++c) acc += part[c];
+#pragma unroll
+    for (int c = 0; c < SPFOM_SPREAD_C; ++c)
+        if (c < S.spread_c) S.spread[(size_t)c * S.spread_n + j] = 0.0;
+    return acc;
+}
+
 __device__ __forceinline__ void dual_update(const DevState &S, int64_t j, int32_t full, int64_t t_next) {
     double acc = S.s[j];
-    if (S.fold_in_dual && j < S.spread_n) {
-        for (int c = 0; c < S.spread_c; ++c) {   // fixed order: deterministic fold of K1's spread copies
-            acc += S.spread[(size_t)c * S.spread_n + j];
-            S.spread[(size_t)c * S.spread_n + j] = 0.0;
-        }
-    }
+    if (S.fold_in_dual && j < S.spread_n) acc = fold_spread(S, j, acc);
     const double sn = full ? acc : S.s_prev[j] + acc;
     const double sx = fma(S.omega_x, sn - S.s_prev[j], sn);
     const double tj = S.tau[j];
@@ -70,12 +81,7 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int
 __global__ void __launch_bounds__(kThreads) k_bundle_usage(DevState S, int32_t full) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x) {
         double acc = S.s[j];
-        if (S.fold_in_dual && j < S.spread_n) {
-            for (int c = 0; c < S.spread_c; ++c) {
-                acc += S.spread[(size_t)c * S.spread_n + j];
-                S.spread[(size_t)c * S.spread_n + j] = 0.0;
-            }
-        }
+        if (S.fold_in_dual && j < S.spread_n) acc = fold_spread(S, j, acc);
         const double sn = full ? acc : S.s_prev[j] + acc;
         S.stilde[j] = fma(S.omega_x, sn - S.s_prev[j], sn);
         S.s_prev[j] = sn;
@@ -147,12 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_resid_res(DevState S, const double
 __global__ void __launch_bounds__(kThreads) k_fold(DevState S) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= S.spread_n) return;
-    double acc = S.s[j];
-    for (int c = 0; c < S.spread_c; ++c) {
-        acc += S.spread[(size_t)c * S.spread_n + j];
-        S.spread[(size_t)c * S.spread_n + j] = 0.0;
-    }
-    S.s[j] = acc;
+    S.s[j] = fold_spread(S, j, S.s[j]);
 }
 
 // ----------------------------------------------------------------- small regime

@@ -612,11 +612,16 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         __syncwarp();
         if (q1 >= 0) issue(q1, qn, q2);
 
-        // a2: price gather (g[N] = 0 for pads; head from shared memory)
+        // a2: price gather (g[N] = 0 for pads; head from shared memory).  The
+        // opaque copies keep the two bases in registers (otherwise ptxas
+        // rebuilds the shared window base and reloads S.g for every entry).
+        uint32_t gh_s = ghead_s;
+        const double *gglob = S.g;
+        asm volatile("" : "+r"(gh_s), "+l"(gglob));
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
-            const double gj = (j < HG) ? lds_f64(ghead_s + 8u * (uint32_t)j) : __ldg(S.g + j);
+            const double gj = (j < HG) ? lds_f64(gh_s + 8u * (uint32_t)j) : __ldg(gglob + j);
             if constexpr (ARGMAX) z[e] = gj;             // theta = inf: keep g itself
             else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
         }
