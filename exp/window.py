@@ -7,7 +7,8 @@ import torch
 from paper_2602_22421_b200 import Params, Solver
 
 lib = None
-inst = bench.load_instance("huge", "/tmp/spfom_cache")
+import os
+inst = bench.load_instance(os.environ.get("CFG", "huge"), "/tmp/spfom_cache")
 s = Solver(inst, Params.converge(), device="cuda:0")
 win, total = int(sys.argv[1]) if len(sys.argv) > 1 else 200, int(sys.argv[2]) if len(sys.argv) > 2 else 2000
 done = 0

@@ -6,7 +6,8 @@ import numpy as np
 import bench
 from paper_2602_22421_b200 import Params, Solver, load_library
 
-inst = bench.load_instance("huge", "/tmp/spfom_cache")
+import os
+inst = bench.load_instance(os.environ.get("CFG", "huge"), "/tmp/spfom_cache")
 s = Solver(inst, Params.converge(), device="cuda:0")
 L = load_library()
 buf = np.zeros(2 * 148 * 8, dtype=np.uint64)

@@ -301,8 +301,8 @@ void launch_mp(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
     L.hh = 0;
     constexpr int W = MPLayout<G, Q>::WARPS;
-    const int64_t units = (L.count + MPLayout<G, Q>::GPW - 1) / MPLayout<G, Q>::GPW * S.T;
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (units + W - 1) / W));
+    const int64_t rounds = (L.count + MPLayout<G, Q>::GPW - 1) / MPLayout<G, Q>::GPW;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
     k_primal_mp<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
@@ -412,12 +412,9 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 // (forked streams; inside a graph they become parallel branches)
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
                 cudaStream_t st = h->nbins_active > 1 ? h->side[b] : h->stream;
-                if (h->T > 1) {
-                    mp_dispatch(b, argmax, S, SL, sms, st);
-                } else {
-                    CUDA_TRY(h, cudaMemsetAsync(SL.work, 0, 8, st));   // dynamic round chunks start at 0
-                    stream_dispatch(b, argmax, S, SL, sms, st);
-                }
+                CUDA_TRY(h, cudaMemsetAsync(SL.work, 0, 8, st));   // dynamic round chunks start at 0
+                if (h->T > 1) mp_dispatch(b, argmax, S, SL, sms, st);
+                else stream_dispatch(b, argmax, S, SL, sms, st);
                 ++nl;
                 continue;
             }

@@ -139,7 +139,7 @@ __device__ __forceinline__ double y_entry(double z, double v, double om, double 
 
 #ifdef SPFOM_DIAG_TIME
 __device__ uint64_t g_diag_time[2 * 148 * 16];   // diagnostic: per-warp start / end of the last K1 launch
-__device__ uint32_t g_diag_loops[148 * 16];      // diagnostic: Newton loop trips per warp (cumulative)
+__device__ uint32_t g_diag_loops[4 * 148 * 16];  // diagnostic: per warp: mbarrier-wait, scatter kcycles, smid
 #endif
 struct ProjStats {
     unsigned long long passes = 0, failures = 0, restarts = 0;
@@ -168,7 +168,7 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
     const int restart_at = max_newton / 2;
     while (__any_sync(0xffffffffu, go)) {
 #ifdef SPFOM_DIAG_TIME
-        g_diag_loops[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] += ((threadIdx.x & 31) == 0);
+        if ((threadIdx.x & 31) == 0) g_diag_loops[4 * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) + 3] += 1u;
 #endif
         // safeguard: a segment still unconverged after half the budget restarts
         // from the cold point (nu, kappa, U) = ((z0 + sum z - lam)/(k+1), 0, lam/(vt0 + sum vt))
@@ -365,6 +365,9 @@ __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 #ifndef SPFOM_DYN_CH
 #define SPFOM_DYN_CH 2   // rounds per dynamically claimed chunk (0: static contiguous partition per warp)
 #endif
+#ifndef SPFOM_DYN_CH_MP
+#define SPFOM_DYN_CH_MP 1   // multi-period kernel: rounds (x T periods) per dynamically claimed chunk
+#endif
 #ifndef SPFOM_HIST_TOTAL_E
 #define SPFOM_HIST_TOTAL_E SPFOM_HIST_TOTAL   // entry-mapped layouts have a smaller slot: room for more
 #endif
@@ -467,6 +470,9 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 #ifdef SPFOM_DIAG_TIME
     uint64_t t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    long long wait_cycles = 0, red_cycles = 0;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
 #endif
 
     // Rounds of GPW consecutive segments.  SPFOM_DYN_CH > 0: warps claim
@@ -550,7 +556,14 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     uint32_t phase = 0;
     for (; q0 >= 0; q0 = q1, q1 = q2, q2 = fnext(), phase ^= 1u) {
         const int64_t r = q0;
+#ifdef SPFOM_DIAG_TIME
+        const long long tw0 = clock64();
         mbar_wait(bar, phase);
+        wait_cycles += clock64() - tw0;
+        const long long tr0 = clock64();
+#else
+        mbar_wait(bar, phase);
+#endif
         // round q1's offsets from the window that arrived with this round
         int32_t qn = 0;
         if (q1 >= 0) {
@@ -646,6 +659,9 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             if (q < qb) st256_stream(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+#ifdef SPFOM_DIAG_TIME
+        const long long ts0 = clock64();
+#endif
         // a5: head -> histogram, warm head -> spread copies, tail -> s
         // ids are distinct within a segment and every group has its own
         // histogram: all loads first, then all stores (no serial RMW chain)
@@ -663,10 +679,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             const int off = j < spread_n ? spread_rel + j : j;     // warm head -> this warp's spread copy
             red_add_if(S.s + off, yv[e], j >= HH && j < N);
         }
+#ifdef SPFOM_DIAG_TIME
+        red_cycles += clock64() - ts0;
+        (void)tr0;
+#endif
         qc = qn;
     }
 #ifdef SPFOM_DIAG_TIME
     if (lane == 0) {
+        g_diag_loops[4 * (blockIdx.x * LY::WARPS + warp)] = (uint32_t)(wait_cycles >> 10);
+        g_diag_loops[4 * (blockIdx.x * LY::WARPS + warp) + 1] = (uint32_t)(red_cycles >> 10);
+        g_diag_loops[4 * (blockIdx.x * LY::WARPS + warp) + 2] = smid;
         uint64_t t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         g_diag_time[2 * (blockIdx.x * LY::WARPS + warp)] = t_start;
@@ -777,24 +800,51 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
     }
     __syncthreads();
 
-    const int64_t rounds = (L.count + GPW - 1) / GPW;
-    const int64_t units = rounds * T;
-    const int64_t W = (int64_t)gridDim.x * LY::WARPS;
-    const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
-    const int64_t u0 = units * gw / W, u1 = units * (gw + 1) / W;
+    // Whole rounds (all T periods of GPW base segments) per claim: warps take
+    // rounds from a global counter (SPFOM_DYN_CH_MP > 0; see k_primal_stream)
+    // or a static contiguous split; q0 / q1 / q2 as in k_primal_stream.
+    const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
+    constexpr int CH = SPFOM_DYN_CH_MP;
+    const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
+    auto grab = [&]() -> int32_t {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(L.work, 1ull);
+        return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
+    };
+    int32_t fpos = 0, fend = 0, fpend = 0;
+    if constexpr (CH > 0) {
+        fpend = grab();
+    } else {
+        const int64_t W = (int64_t)gridDim.x * LY::WARPS;
+        const int64_t gw = (int64_t)blockIdx.x * LY::WARPS + warp;
+        fpos = (int32_t)(rounds * gw / W);
+        fend = (int32_t)(rounds * (gw + 1) / W);
+    }
+    auto fnext = [&]() -> int32_t {
+        if constexpr (CH > 0) {
+            if (fpos >= fend) {
+                if (fpend >= nch) return -1;
+                fpos = fpend * CH;
+                fend = min(fpos + CH, rounds);
+                fpend = grab();
+            }
+        } else {
+            if (fpos >= fend) return -1;
+        }
+        return fpos++;
+    };
 
     auto qload = [&](int64_t r) -> int32_t {
         int64_t k = GPW * r + (lane < GPW ? lane : GPW);
         k = k < L.count ? k : L.count;
         return S.qoff[L.first + k];
     };
-    // structure of round r (+ the qoff window of round r + 1)
-    auto issueS = [&](int64_t r, int32_t q, bool window) {
+    // structure of round r (+ the qoff window of round rw >= 0)
+    auto issueS = [&](int64_t r, int32_t q, int64_t rw) {
         const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
-        const int64_t s0 = L.first + GPW * r;
         const uint32_t nq = (uint32_t)(qb - qa);
-        const int64_t w0 = (s0 + GPW) & ~(int64_t)3;
-        const uint32_t wbytes = window ? 4u * LY::QW : 0u;
+        const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;
+        const uint32_t wbytes = rw >= 0 ? 4u * LY::QW : 0u;
         if (lane == 0) {
             mbar_arrive_expect_tx(barS, 80u * nq + wbytes);
             if (wbytes) bulk_g2s(ws + LY::S_QW, S.qoff + w0, wbytes, barS);
@@ -822,121 +872,113 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
 
     ProjStats st;
     int32_t qc = 0, qn = 0;
-    if (u0 < u1) {
-        const int64_t r = u0 / T;
-        qc = qload(r);
-        issueS(r, qc, (r + 1) * T < u1);
-        issueP(r, u0 % T, qc);
+    int32_t q0 = fnext(), q1 = fnext(), q2 = fnext();
+    if (q0 >= 0) {
+        qc = qload(q0);
+        issueS(q0, qc, q1);
+        issueP(q0, 0, qc);
     }
     uint32_t phS = 0, phP = 0;
-    int64_t rprev = -1;
     int idx[NE];
     double v[NE], om[NE];
-    int32_t qa = 0, qb = 0, base = 0;
-    for (int64_t u = u0; u < u1; ++u) {
-        const int64_t r = u / T, t = u - r * T;
-        if (r != rprev) {
-            // ---- new round: structure into registers, theta g into shared memory
-            mbar_wait(barS, phS);
-            phS ^= 1u;
-            if ((r + 1) * T < u1) {
-                const int64_t s1 = L.first + GPW * (r + 1);
-                int64_t k = GPW * (r + 1) + (lane < GPW ? lane : GPW);
-                k = k < L.count ? k : L.count;
-                qn = reinterpret_cast<const int32_t *>(ws + LY::S_QW)[L.first + k - (s1 & ~(int64_t)3)];
-            }
-            base = __shfl_sync(0xffffffffu, qc, 0);
-            qa = __shfl_sync(0xffffffffu, qc, gidx);
-            qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
-#pragma unroll
-            for (int tq = 0; tq < Q; ++tq) {
-                const int32_t q = qa + gl + G * tq;
-                const int p = q < qb ? q - base : LY::QMAX;
-                const int4 id4 = reinterpret_cast<const int4 *>(ws + LY::S_IDS)[p];
-                idx[4 * tq + 0] = id4.x; idx[4 * tq + 1] = id4.y; idx[4 * tq + 2] = id4.z; idx[4 * tq + 3] = id4.w;
-                const double2 *vp = reinterpret_cast<const double2 *>(ws + LY::S_V) + 2 * p;
-                const double2 *wp = reinterpret_cast<const double2 *>(ws + LY::S_OM) + 2 * p;
-                const double2 v01 = vp[0], v23 = vp[1], w01 = wp[0], w23 = wp[1];
-                v[4 * tq + 0] = v01.x; v[4 * tq + 1] = v01.y; v[4 * tq + 2] = v23.x; v[4 * tq + 3] = v23.y;
-                om[4 * tq + 0] = w01.x; om[4 * tq + 1] = w01.y; om[4 * tq + 2] = w23.x; om[4 * tq + 3] = w23.y;
-            }
-            __syncwarp();                                  // slot reads before the copy (see k_primal_stream)
-            if ((r + 1) * T < u1) issueS(r + 1, qn, (r + 2) * T < u1);
-#pragma unroll
-            for (int e = 0; e < NE; ++e) {
-                const int j = idx[e];
-                const double gj = (j < HG) ? lds_f64(ghead_s + 8u * (uint32_t)j) : __ldg(S.g + j);
-                sts_f64(gt_s + 256u * e, ARGMAX ? gj : S.theta * gj);   // a2 (+ the theta of a3)
-                sts_f64(ys_s + 256u * e, 0.0);
-            }
-            rprev = r;
+    for (; q0 >= 0; q0 = q1, q1 = q2, q2 = fnext()) {
+        const int64_t r = q0;
+        // ---- new round: structure into registers, theta g into shared memory
+        mbar_wait(barS, phS);
+        phS ^= 1u;
+        qn = 0;
+        if (q1 >= 0) {
+            const int64_t s1 = L.first + GPW * (int64_t)q1;
+            int64_t k = GPW * (int64_t)q1 + (lane < GPW ? lane : GPW);
+            k = k < L.count ? k : L.count;
+            qn = reinterpret_cast<const int32_t *>(ws + LY::S_QW)[L.first + k - (s1 & ~(int64_t)3)];
         }
-        // ---- period t of round r
-        mbar_wait(barP, phP);
-        phP ^= 1u;
-        const int64_t left = L.count - GPW * r;
-        const bool active = gidx < left;
-        const int64_t i = L.first + GPW * r + gidx;      // device base slot
-        double lam = 1.0, vt0 = 1.0;
-        double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
-        if (active) {
-            sv = reinterpret_cast<const double4 *>(ws + LY::P_SEGV)[gidx];
-            const double2 sc = reinterpret_cast<const double2 *>(ws + LY::P_SEGC)[gidx];
-            lam = sc.x;
-            vt0 = sc.y;
-        }
-        double z[NE];
+        const int32_t base = __shfl_sync(0xffffffffu, qc, 0);
+        const int32_t qa = __shfl_sync(0xffffffffu, qc, gidx);
+        const int32_t qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
 #pragma unroll
         for (int tq = 0; tq < Q; ++tq) {
             const int32_t q = qa + gl + G * tq;
             const int p = q < qb ? q - base : LY::QMAX;
-            const double2 *yp = reinterpret_cast<const double2 *>(ws + LY::P_Y) + 2 * p;
-            const double2 y01 = yp[0], y23 = yp[1];
-            z[4 * tq + 0] = y01.x; z[4 * tq + 1] = y01.y; z[4 * tq + 2] = y23.x; z[4 * tq + 3] = y23.y;
+            const int4 id4 = reinterpret_cast<const int4 *>(ws + LY::S_IDS)[p];
+            idx[4 * tq + 0] = id4.x; idx[4 * tq + 1] = id4.y; idx[4 * tq + 2] = id4.z; idx[4 * tq + 3] = id4.w;
+            const double2 *vp = reinterpret_cast<const double2 *>(ws + LY::S_V) + 2 * p;
+            const double2 *wp = reinterpret_cast<const double2 *>(ws + LY::S_OM) + 2 * p;
+            const double2 v01 = vp[0], v23 = vp[1], w01 = wp[0], w23 = wp[1];
+            v[4 * tq + 0] = v01.x; v[4 * tq + 1] = v01.y; v[4 * tq + 2] = v23.x; v[4 * tq + 3] = v23.y;
+            om[4 * tq + 0] = w01.x; om[4 * tq + 1] = w01.y; om[4 * tq + 2] = w23.x; om[4 * tq + 3] = w23.y;
         }
-        __syncwarp();
-        if (u + 1 < u1) {
-            const int64_t rn = (u + 1) / T;
-            issueP(rn, (u + 1) - rn * T, rn == r ? qc : qn);
-        }
+        __syncwarp();                                  // slot reads before the copy (see k_primal_stream)
+        if (q1 >= 0) issueS(q1, qn, q2);
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            const double gt = lds_f64_v(gt_s + 256u * e);
-            z[e] = ARGMAX ? gt : z[e] + gt;                  // a3: z = y + theta g
+            const int j = idx[e];
+            const double gj = (j < HG) ? lds_f64(ghead_s + 8u * (uint32_t)j) : __ldg(S.g + j);
+            sts_f64(gt_s + 256u * e, ARGMAX ? gj : S.theta * gj);   // a2 (+ the theta of a3)
+            sts_f64(ys_s + 256u * e, 0.0);
         }
-        double yv[NE];
-        double y0new;
-        double x0 = sv.y, x1 = sv.z, x2 = sv.w;
-        if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
-        else project_group<G, NE>(z, v, om, sv.x, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
-
-        // ---- write back y_t and the segment state; accumulate sum_t y
+        const int64_t left = L.count - GPW * r;
+        const bool active = gidx < left;
+        const int64_t i = L.first + GPW * r + gidx;      // device base slot
+        for (int64_t t = 0; t < T; ++t) {
+            // ---- period t of round r
+            mbar_wait(barP, phP);
+            phP ^= 1u;
+            double lam = 1.0, vt0 = 1.0;
+            double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
+            if (active) {
+                sv = reinterpret_cast<const double4 *>(ws + LY::P_SEGV)[gidx];
+                const double2 sc = reinterpret_cast<const double2 *>(ws + LY::P_SEGC)[gidx];
+                lam = sc.x;
+                vt0 = sc.y;
+            }
+            double z[NE];
 #pragma unroll
-        for (int tq = 0; tq < Q; ++tq) {
-            const int32_t q = qa + gl + G * tq;
-            if (q < qb)
-                st256(S.y + 4 * (t * nqb + q), yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
-        }
-        if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
-#pragma unroll
-        {
-            double hv[NE];                                 // loads first: no serial RMW chain
-#pragma unroll
-            for (int e = 0; e < NE; ++e) hv[e] = lds_f64_v(ys_s + 256u * e);
-#pragma unroll
-            for (int e = 0; e < NE; ++e) sts_f64(ys_s + 256u * e, hv[e] + yv[e]);
-        }
-
-        // ---- end of this warp's part of round r: a5 scatter of sum_t y
-        if (u + 1 == u1 || (u + 1) / T != r) {
+            for (int tq = 0; tq < Q; ++tq) {
+                const int32_t q = qa + gl + G * tq;
+                const int p = q < qb ? q - base : LY::QMAX;
+                const double2 *yp = reinterpret_cast<const double2 *>(ws + LY::P_Y) + 2 * p;
+                const double2 y01 = yp[0], y23 = yp[1];
+                z[4 * tq + 0] = y01.x; z[4 * tq + 1] = y01.y; z[4 * tq + 2] = y23.x; z[4 * tq + 3] = y23.y;
+            }
+            __syncwarp();
+            if (t + 1 < T) issueP(r, t + 1, qc);
+            else if (q1 >= 0) issueP(q1, 0, qn);
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
-                const int j = idx[e];
-                const int off = j < spread_n ? spread_rel + j : j;
-                red_add_if(S.s + off, lds_f64_v(ys_s + 256u * e), j < N);
+                const double gt = lds_f64_v(gt_s + 256u * e);
+                z[e] = ARGMAX ? gt : z[e] + gt;                  // a3: z = y + theta g
             }
-            qc = qn;
+            double yv[NE];
+            double y0new;
+            double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+            if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
+            else project_group<G, NE>(z, v, om, sv.x, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
+
+            // ---- write back y_t and the segment state; accumulate sum_t y
+#pragma unroll
+            for (int tq = 0; tq < Q; ++tq) {
+                const int32_t q = qa + gl + G * tq;
+                if (q < qb)
+                    st256(S.y + 4 * (t * nqb + q), yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
+            }
+            if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
+            {
+                double hv[NE];                                 // loads first: no serial RMW chain
+#pragma unroll
+                for (int e = 0; e < NE; ++e) hv[e] = lds_f64_v(ys_s + 256u * e);
+#pragma unroll
+                for (int e = 0; e < NE; ++e) sts_f64(ys_s + 256u * e, hv[e] + yv[e]);
+            }
         }
+        // ---- end of round r: a5 scatter of sum_t y
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int j = idx[e];
+            const int off = j < spread_n ? spread_rel + j : j;
+            red_add_if(S.s + off, lds_f64_v(ys_s + 256u * e), j < N);
+        }
+        qc = qn;
     }
     if constexpr (!ARGMAX) {
         if (st.passes) {
