@@ -123,6 +123,10 @@ constexpr int kSpreadCopies = SPFOM_SPREAD_C;
 int64_t spread_range(int64_t N) { return kSpreadCopies > 0 ? std::min<int64_t>(N, SPFOM_SPREAD_N) : 0; }
 int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spread slot after the N + 1 acc slots
 
+// pinned staging ring of a handle: 2 buffers of kPinQuads quads x 80 B (ids +
+// v + omega at create; the getters' D2H uses 32 B per quad of it)
+constexpr int64_t kPinQuads = (int64_t)1 << 18;
+
 int64_t recover_chunk(int64_t nq) { return std::min<int64_t>(std::max<int64_t>(4 * nq, 4096), (int64_t)1 << 22); }
 
 void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
@@ -200,6 +204,9 @@ struct spfom_handle {
     std::unique_ptr<int64_t[]> pos_map;        // original entry -> padded entry [nnz] (no zero-fill)
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
+    std::vector<int32_t> qoff_h;               // device-order quad offsets [m + 1] (host copy)
+    double *pin[2] = {nullptr, nullptr};       // pinned D2H staging ring (getters), allocated on first use
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
@@ -713,6 +720,11 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             if (h->ev_join[b]) cudaEventDestroy(h->ev_join[b]);
         }
         if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+        for (int c = 0; c < 2; ++c) {
+            if (h->pin_ev[c]) cudaEventSynchronize(h->pin_ev[c]);
+            if (h->pin[c]) cudaFreeHost(h->pin[c]);
+            if (h->pin_ev[c]) cudaEventDestroy(h->pin_ev[c]);
+        }
         if (h->own_stream) cudaStreamDestroy(h->stream);
         delete h;
         return s;
@@ -732,7 +744,14 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     ptimer.mark("plan+handle+streams");
     // ---- global column counts n_j
     std::vector<int64_t> counts(N + 1, 0);
-    for (int64_t e = 0; e < in->nnz; ++e) counts[in->prod_idx[e]] += h->T;   // stacked segments (T per base row)
+#pragma omp parallel
+    {
+        std::vector<int64_t> loc(N + 1, 0);                    // per-thread histogram, merged below
+#pragma omp for schedule(static) nowait
+        for (int64_t e = 0; e < in->nnz; ++e) loc[in->prod_idx[e]] += h->T;   // stacked segments (T per base row)
+#pragma omp critical
+        for (int64_t j = 0; j <= N; ++j) counts[j] += loc[j];
+    }
     if (h->world > 1) {
         int64_t *dcounts = slot_ptr<int64_t>(h, O_COUNTS);
         if (cudaMemcpyAsync(dcounts, counts.data(), N * 8, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D counts"; return bail(SPFOM_ECUDA); }
@@ -824,55 +843,99 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         qoff[k + 1] = qoff[k] + (int32_t)((in->seg_ptr[i + 1] - in->seg_ptr[i] + 3) / 4);
     }
     const int64_t nq = qoff[m];
-    // uninitialised host staging (the parallel loop writes every padded slot, pads included)
-    std::unique_ptr<int32_t[]> pidx(new int32_t[4 * std::max<int64_t>(nq, 1)]);
-    std::unique_ptr<double[]> vv(new double[4 * std::max<int64_t>(nq, 1)]), om(new double[4 * std::max<int64_t>(nq, 1)]);
     const int64_t T = h->T;
     std::vector<double2> segc(std::max<int64_t>(T * m, 1));
     std::vector<double4> segv(std::max<int64_t>(T * m, 1));
     h->pos_map.reset(new int64_t[std::max<int64_t>(in->nnz, 1)]);
     h->seg_off.assign(in->seg_ptr, in->seg_ptr + m + 1);
     bool bad_numeric = false;
+    // The padded arrays (ids, v, omega) are built chunk by chunk of device
+    // slots straight into a pinned double buffer and copied to the workspace
+    // asynchronously, so chunk c + 1 is built while chunk c is in flight (no
+    // pageable staging of the whole instance, no serial H2D afterwards).  The
+    // same pinned ring later stages the getters' D2H copies.
+    for (int c = 0; c < 2; ++c) {
+        if (cudaMallocHost(reinterpret_cast<void **>(&h->pin[c]), kPinQuads * 80) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->pin_ev[c], cudaEventDisableTiming) != cudaSuccess) {
+            h->err = "pinned staging";
+            return bail(SPFOM_ENOMEM);
+        }
+    }
+    char *d_pidx = h->ws + h->pl.off[O_PIDX], *d_v = h->ws + h->pl.off[O_V], *d_om = h->ws + h->pl.off[O_OM];
+    bool copy_ok = true;
+    int64_t chunk_no = 0;
+    for (int64_t k0 = 0; k0 < m;) {
+        int64_t k1 = k0 + 1;
+        while (k1 < m && (int64_t)qoff[k1 + 1] - qoff[k0] <= kPinQuads) ++k1;
+        const int64_t q0 = qoff[k0], nqc = (int64_t)qoff[k1] - q0;
+        std::vector<char> big;                                   // a single row longer than a buffer
+        char *buf;
+        if (nqc > kPinQuads) {
+            big.resize(nqc * 80);
+            buf = big.data();
+        } else {
+            const int c = (int)(chunk_no & 1);
+            if (chunk_no >= 2 && cudaEventSynchronize(h->pin_ev[c]) != cudaSuccess) copy_ok = false;   // buffer free again
+            buf = reinterpret_cast<char *>(h->pin[c]);
+        }
+        int32_t *pidx = reinterpret_cast<int32_t *>(buf);                 // [4 nqc]
+        double *vv = reinterpret_cast<double *>(buf + 16 * nqc);           // [4 nqc]
+        double *om = reinterpret_cast<double *>(buf + 48 * nqc);           // [4 nqc]
+        const int64_t pbase = 4 * q0;
 #pragma omp parallel
-    {
-    std::vector<std::pair<int32_t, int64_t>> order;                 // per-thread sort buffer
-#pragma omp for schedule(dynamic, 4096)
-    for (int64_t k = 0; k < m; ++k) {
-        const int64_t i = h->sorder[k];
-        const int64_t a = in->seg_ptr[i], len = in->seg_ptr[i + 1] - a;
-        order.resize(len);
-        for (int64_t q = 0; q < len; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
-        std::sort(order.begin(), order.end());
-        const int64_t pend = 4 * (int64_t)qoff[k + 1];
-        for (int64_t p = 4 * (int64_t)qoff[k] + len; p < pend; ++p) {   // inert pads
-            pidx[p] = (int32_t)N;
-            vv[p] = 0.0;
-            om[p] = 0.0;
+        {
+        std::vector<std::pair<int32_t, int64_t>> order;                 // per-thread sort buffer
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t i = h->sorder[k];
+            const int64_t a = in->seg_ptr[i], len = in->seg_ptr[i + 1] - a;
+            order.resize(len);
+            for (int64_t q = 0; q < len; ++q) order[q] = {h->old2new[in->prod_idx[a + q]], a + q};
+            std::sort(order.begin(), order.end());
+            const int64_t pend = 4 * (int64_t)qoff[k + 1] - pbase;
+            for (int64_t p = 4 * (int64_t)qoff[k] - pbase + len; p < pend; ++p) {   // inert pads
+                pidx[p] = (int32_t)N;
+                vv[p] = 0.0;
+                om[p] = 0.0;
+            }
+            double vt0 = in->no_purchase[i], svt = 0.0;
+            const int64_t base = 4 * (int64_t)qoff[k];
+            for (int64_t q = 0; q < len; ++q) {
+                const int64_t e = order[q].second;
+                const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
+                pidx[base - pbase + q] = order[q].first;
+                vv[base - pbase + q] = v;
+                om[base - pbase + q] = w / v;
+                vt0 += w;
+                svt += v - w;
+                h->pos_map[e] = base + q;
+            }
+            for (int64_t t = 0; t < T; ++t) {
+                const double lam = in->arrival[t * m + i];
+                segc[t * m + k] = make_double2(lam, vt0);
+                // y0 = lambda and the initial projection multipliers (nu, kappa, U)
+                segv[t * m + k] = make_double4(lam, 0.0, 0.0, lam / (vt0 + svt));
+            }
+            if (!std::isfinite(vt0)) bad_numeric = true;
         }
-        double vt0 = in->no_purchase[i], svt = 0.0;
-        const int64_t base = 4 * (int64_t)qoff[k];
-        for (int64_t q = 0; q < len; ++q) {
-            const int64_t e = order[q].second;
-            const double v = in->attract[e], w = in->shadow ? in->shadow[e] : 0.0;
-            pidx[base + q] = order[q].first;
-            vv[base + q] = v;
-            om[base + q] = w / v;
-            vt0 += w;
-            svt += v - w;
-            h->pos_map[e] = base + q;
         }
-        for (int64_t t = 0; t < T; ++t) {
-            const double lam = in->arrival[t * m + i];
-            segc[t * m + k] = make_double2(lam, vt0);
-            // y0 = lambda and the initial projection multipliers (nu, kappa, U)
-            segv[t * m + k] = make_double4(lam, 0.0, 0.0, lam / (vt0 + svt));
+        if (nqc > 0) {
+            copy_ok = copy_ok && cudaMemcpyAsync(d_pidx + 16 * q0, pidx, nqc * 16, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+                      cudaMemcpyAsync(d_v + 32 * q0, vv, nqc * 32, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+                      cudaMemcpyAsync(d_om + 32 * q0, om, nqc * 32, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
         }
-        if (!std::isfinite(vt0)) bad_numeric = true;
+        if (nqc > kPinQuads) {
+            if (cudaStreamSynchronize(h->stream) != cudaSuccess) copy_ok = false;   // `big` goes out of scope
+        } else {
+            if (cudaEventRecord(h->pin_ev[chunk_no & 1], h->stream) != cudaSuccess) copy_ok = false;
+            ++chunk_no;
+        }
+        k0 = k1;
     }
-    }
-    if (nq == 0) { pidx[0] = (int32_t)N; vv[0] = 0.0; om[0] = 0.0; }
+    if (!copy_ok) { h->err = "H2D copy of the padded CSR failed"; return bail(SPFOM_ECUDA); }
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
 
+    h->qoff_h = qoff;
     ptimer.mark("padded CSR (omp)");
     // ---- sampled block tables: per (iteration, bin) lists of device slots
     if (pl.sampled) {
@@ -915,8 +978,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     };
     std::vector<double> y0(std::max<int64_t>(T * m, 1));
     for (int64_t k = 0; k < T * m; ++k) y0[k] = segv[k].x;
-    bool ok = H2D(O_PIDX, pidx.get(), nq * 16) && H2D(O_V, vv.get(), nq * 32) && H2D(O_OM, om.get(), nq * 32) &&
-              H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
+    bool ok = H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
               H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), D1 * 8) &&
               H2D(O_TAU, tau.data(), D1 * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
               H2D(O_ORIG, h->new2old.data(), N * 4);
@@ -1144,27 +1206,77 @@ spfom_status spfom_usage(spfom_handle *h, double *s) {
 }
 
 // y0 in device order is either a plain array (pitch 8) or the x field of segv (pitch 32)
-// y: device [T][nq] quads -> [T][nnz] stacked entry order
+// y: device [T][nq] quads -> [T][nnz] stacked entry order.  The quads come
+// down in chunks of device slots through a pinned double buffer: chunk c + 1
+// copies (full PCIe rate) while the host un-permutes chunk c into y (rows of
+// the slots' original segments; pos_map gives each entry's padded position).
 static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double *dy0, size_t pitch0, double *y,
                                  double *y0) {
-    const int64_t T = h->T;
-    std::unique_ptr<double[]> tmp(new double[4 * std::max<int64_t>(T * h->nq, 1)]);   // no zero-fill
-    std::vector<double> t0(std::max<int64_t>(T * h->m, 1));
-    if (y && h->nq) CUDA_TRY(h, cudaMemcpyAsync(tmp.get(), dy, T * h->nq * 32, cudaMemcpyDeviceToHost, h->stream));
-    if (y0 && h->m)
-        CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, T * h->m, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-    for (int64_t t = 0; t < T; ++t) {
-        if (y) {
-            const int64_t *pm = h->pos_map.get();
-            const double *src = tmp.get() + 4 * t * h->nq;
-            double *dst = y + t * h->nnz;
-#pragma omp parallel for schedule(static)
-            for (int64_t e = 0; e < h->nnz; ++e) dst[e] = src[pm[e]];
+    const int64_t T = h->T, m = h->m;
+    std::vector<double> t0(std::max<int64_t>(T * m, 1));
+    if (y0 && m)
+        CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, T * m, cudaMemcpyDeviceToHost, h->stream));
+    if (y && h->nq) {
+        for (int c = 0; c < 2; ++c) {
+            if (!h->pin[c]) CUDA_TRY(h, cudaMallocHost(reinterpret_cast<void **>(&h->pin[c]), kPinQuads * 80));
+            if (!h->pin_ev[c]) CUDA_TRY(h, cudaEventCreateWithFlags(&h->pin_ev[c], cudaEventDisableTiming));
         }
-        if (y0)
-            for (int64_t k = 0; k < h->m; ++k) y0[t * h->m + h->sorder[k]] = t0[t * h->m + k];
+        // chunks: (period t, device slots [k0, k1)) with at most kPinQuads quads
+        // (a longer single row gets a chunk of its own, copied in pieces below)
+        struct Chunk { int64_t t, k0, k1; };
+        std::vector<Chunk> chunks;
+        const int32_t *qo = h->qoff_h.data();
+        for (int64_t t = 0; t < T; ++t) {
+            int64_t k0 = 0;
+            while (k0 < m) {
+                int64_t k1 = k0 + 1;
+                while (k1 < m && (int64_t)qo[k1 + 1] - qo[k0] <= kPinQuads) ++k1;
+                chunks.push_back({t, k0, k1});
+                k0 = k1;
+            }
+        }
+        const int64_t *pm = h->pos_map.get();
+        const double *pin_of[2] = {h->pin[0], h->pin[1]};
+        auto issue = [&](size_t c) -> spfom_status {
+            const Chunk &ch = chunks[c];
+            const int64_t q0 = qo[ch.k0], nqc = (int64_t)qo[ch.k1] - q0;
+            if (nqc > kPinQuads) return SPFOM_OK;    // oversized row: synchronous path below
+            CUDA_TRY(h, cudaMemcpyAsync(h->pin[c & 1], dy + 4 * (ch.t * h->nq + q0), nqc * 32, cudaMemcpyDeviceToHost,
+                                        h->stream));
+            CUDA_TRY(h, cudaEventRecord(h->pin_ev[c & 1], h->stream));
+            return SPFOM_OK;
+        };
+        spfom_status st = chunks.empty() ? SPFOM_OK : issue(0);
+        for (size_t c = 0; c < chunks.size() && st == SPFOM_OK; ++c) {
+            const Chunk &ch = chunks[c];
+            const int64_t q0 = qo[ch.k0], nqc = (int64_t)qo[ch.k1] - q0;
+            std::vector<double> big;
+            const double *src;
+            if (nqc > kPinQuads) {
+                big.resize(4 * nqc);
+                CUDA_TRY(h, cudaMemcpyAsync(big.data(), dy + 4 * (ch.t * h->nq + q0), nqc * 32, cudaMemcpyDeviceToHost,
+                                            h->stream));
+                CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+                src = big.data();
+            } else {
+                CUDA_TRY(h, cudaEventSynchronize(h->pin_ev[c & 1]));
+                src = pin_of[c & 1];
+            }
+            if (c + 1 < chunks.size()) st = issue(c + 1);   // next chunk copies while this one is placed
+            double *dst = y + ch.t * h->nnz;
+            const int64_t base = 4 * q0;
+#pragma omp parallel for schedule(dynamic, 1024)
+            for (int64_t k = ch.k0; k < ch.k1; ++k) {
+                const int64_t i = h->sorder[k];
+                for (int64_t e = h->seg_off[i]; e < h->seg_off[i + 1]; ++e) dst[e] = src[pm[e] - base];
+            }
+        }
+        if (st != SPFOM_OK) return st;
     }
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (y0)
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t k = 0; k < m; ++k) y0[t * m + h->sorder[k]] = t0[t * m + k];
     return SPFOM_OK;
 }
 
@@ -1545,6 +1657,10 @@ void spfom_destroy(spfom_handle *h) {
         if (h->ev_join[b]) cudaEventDestroy(h->ev_join[b]);
     }
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    for (int c = 0; c < 2; ++c) {
+        if (h->pin[c]) cudaFreeHost(h->pin[c]);
+        if (h->pin_ev[c]) cudaEventDestroy(h->pin_ev[c]);
+    }
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
 }
