@@ -203,7 +203,11 @@ spfom_status spfom_workspace_bytes(const spfom_instance *inst, const spfom_param
  * eta = 0, s = 0 (reading c10).  cuda_stream: cudaStream_t; NULL (or the
  * legacy default stream, which cannot be graph-captured) => the handle creates
  * and owns a private non-blocking stream.  workspace: 256-byte aligned device
- * pointer of >= spfom_workspace_bytes() bytes. */
+ * pointer of >= spfom_workspace_bytes() bytes.  The handle also owns a 40 MB
+ * pinned host staging ring (cudaMallocHost): the padded CSR is built into it
+ * chunk by chunk and uploaded while the next chunk is built, and the getters
+ * stage their device->host copies through it.  SPFOM_ENOMEM if it cannot be
+ * allocated. */
 spfom_status spfom_create(const spfom_instance *inst, const spfom_params *params,
                           const spfom_dist *dist, void *cuda_stream, void *workspace,
                           size_t workspace_bytes, spfom_handle **out);
