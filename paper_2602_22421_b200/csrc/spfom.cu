@@ -126,6 +126,7 @@ int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spre
 // pinned staging ring of a handle: 2 buffers of kPinQuads quads x 80 B (ids +
 // v + omega at create; the getters' D2H uses 32 B per quad of it)
 constexpr int64_t kPinQuads = (int64_t)1 << 18;
+static_assert(kPinQuads >= kMaxQuads, "a chunk holds at least one row");
 
 int64_t recover_chunk(int64_t nq) { return std::min<int64_t>(std::max<int64_t>(4 * nq, 4096), (int64_t)1 << 22); }
 
@@ -867,17 +868,10 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     for (int64_t k0 = 0; k0 < m;) {
         int64_t k1 = k0 + 1;
         while (k1 < m && (int64_t)qoff[k1 + 1] - qoff[k0] <= kPinQuads) ++k1;
-        const int64_t q0 = qoff[k0], nqc = (int64_t)qoff[k1] - q0;
-        std::vector<char> big;                                   // a single row longer than a buffer
-        char *buf;
-        if (nqc > kPinQuads) {
-            big.resize(nqc * 80);
-            buf = big.data();
-        } else {
-            const int c = (int)(chunk_no & 1);
-            if (chunk_no >= 2 && cudaEventSynchronize(h->pin_ev[c]) != cudaSuccess) copy_ok = false;   // buffer free again
-            buf = reinterpret_cast<char *>(h->pin[c]);
-        }
+        const int64_t q0 = qoff[k0], nqc = (int64_t)qoff[k1] - q0;   // <= kPinQuads (rows <= kMaxQuads)
+        const int c = (int)(chunk_no & 1);
+        if (chunk_no >= 2 && cudaEventSynchronize(h->pin_ev[c]) != cudaSuccess) copy_ok = false;   // buffer free again
+        char *buf = reinterpret_cast<char *>(h->pin[c]);
         int32_t *pidx = reinterpret_cast<int32_t *>(buf);                 // [4 nqc]
         double *vv = reinterpret_cast<double *>(buf + 16 * nqc);           // [4 nqc]
         double *om = reinterpret_cast<double *>(buf + 48 * nqc);           // [4 nqc]
@@ -924,12 +918,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
                       cudaMemcpyAsync(d_v + 32 * q0, vv, nqc * 32, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
                       cudaMemcpyAsync(d_om + 32 * q0, om, nqc * 32, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
         }
-        if (nqc > kPinQuads) {
-            if (cudaStreamSynchronize(h->stream) != cudaSuccess) copy_ok = false;   // `big` goes out of scope
-        } else {
-            if (cudaEventRecord(h->pin_ev[chunk_no & 1], h->stream) != cudaSuccess) copy_ok = false;
-            ++chunk_no;
-        }
+        if (cudaEventRecord(h->pin_ev[c], h->stream) != cudaSuccess) copy_ok = false;
+        ++chunk_no;
         k0 = k1;
     }
     if (!copy_ok) { h->err = "H2D copy of the padded CSR failed"; return bail(SPFOM_ECUDA); }
@@ -1222,7 +1212,6 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
             if (!h->pin_ev[c]) CUDA_TRY(h, cudaEventCreateWithFlags(&h->pin_ev[c], cudaEventDisableTiming));
         }
         // chunks: (period t, device slots [k0, k1)) with at most kPinQuads quads
-        // (a longer single row gets a chunk of its own, copied in pieces below)
         struct Chunk { int64_t t, k0, k1; };
         std::vector<Chunk> chunks;
         const int32_t *qo = h->qoff_h.data();
@@ -1239,8 +1228,7 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
         const double *pin_of[2] = {h->pin[0], h->pin[1]};
         auto issue = [&](size_t c) -> spfom_status {
             const Chunk &ch = chunks[c];
-            const int64_t q0 = qo[ch.k0], nqc = (int64_t)qo[ch.k1] - q0;
-            if (nqc > kPinQuads) return SPFOM_OK;    // oversized row: synchronous path below
+            const int64_t q0 = qo[ch.k0], nqc = (int64_t)qo[ch.k1] - q0;   // <= kPinQuads
             CUDA_TRY(h, cudaMemcpyAsync(h->pin[c & 1], dy + 4 * (ch.t * h->nq + q0), nqc * 32, cudaMemcpyDeviceToHost,
                                         h->stream));
             CUDA_TRY(h, cudaEventRecord(h->pin_ev[c & 1], h->stream));
@@ -1249,19 +1237,9 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
         spfom_status st = chunks.empty() ? SPFOM_OK : issue(0);
         for (size_t c = 0; c < chunks.size() && st == SPFOM_OK; ++c) {
             const Chunk &ch = chunks[c];
-            const int64_t q0 = qo[ch.k0], nqc = (int64_t)qo[ch.k1] - q0;
-            std::vector<double> big;
-            const double *src;
-            if (nqc > kPinQuads) {
-                big.resize(4 * nqc);
-                CUDA_TRY(h, cudaMemcpyAsync(big.data(), dy + 4 * (ch.t * h->nq + q0), nqc * 32, cudaMemcpyDeviceToHost,
-                                            h->stream));
-                CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-                src = big.data();
-            } else {
-                CUDA_TRY(h, cudaEventSynchronize(h->pin_ev[c & 1]));
-                src = pin_of[c & 1];
-            }
+            const int64_t q0 = qo[ch.k0];
+            CUDA_TRY(h, cudaEventSynchronize(h->pin_ev[c & 1]));
+            const double *src = pin_of[c & 1];
             if (c + 1 < chunks.size()) st = issue(c + 1);   // next chunk copies while this one is placed
             double *dst = y + ch.t * h->nnz;
             const int64_t base = 4 * q0;
