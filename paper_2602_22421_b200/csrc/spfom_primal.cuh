@@ -450,22 +450,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
-    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
-    for (int w = 0; w < LY::WARPS; ++w) {
-        double *h = reinterpret_cast<double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
-        for (int j = threadIdx.x; j < LY::NHIST * HS; j += blockDim.x) h[j] = 0.0;
-    }
-    if (lane < 6) {   // this warp's inert zero quad
-        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[lane] = 0.0;
-        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[lane] = 0.0;
-        if (lane < 4) reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[lane] = 0.0;
-        if (lane < 4) reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[lane] = N;
+    if (lane < 4) {   // this warp's inert zero quad (past the quads the copies write)
+        reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[lane] = 0.0;
+        reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[lane] = 0.0;
+        reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[lane] = 0.0;
+        reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[lane] = N;
     }
     if (lane == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    __syncwarp();
     (void)hist_all;
 #ifdef SPFOM_DIAG_TIME
     uint64_t t_start;
@@ -484,12 +479,19 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
     constexpr int CH = SPFOM_DYN_CH;
     const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
-    auto grab = [&]() -> int32_t {
+    // the claimed chunk id stays in lane 0's register until the warp moves to
+    // that chunk (the broadcast is the first use: the atomic's latency is
+    // hidden behind the current chunk's rounds)
+    auto grab = [&]() -> unsigned long long {
         unsigned long long c = 0;
         if (lane == 0) c = atomicAdd(L.work, 1ull);
+        return c;
+    };
+    auto bcast = [&](unsigned long long c) -> int32_t {
         return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
     };
-    int32_t fpos = 0, fend = 0, fpend = 0;
+    int32_t fpos = 0, fend = 0;
+    unsigned long long fpend = 0;
     if constexpr (CH > 0) {
         fpend = grab();
     } else {
@@ -501,8 +503,9 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     auto fnext = [&]() -> int32_t {
         if constexpr (CH > 0) {
             if (fpos >= fend) {
-                if (fpend >= nch) return -1;
-                fpos = fpend * CH;
+                const int32_t c = bcast(fpend);
+                if (c >= nch) return -1;
+                fpos = c * CH;
                 fend = min(fpos + CH, rounds);
                 fpend = grab();
             }
@@ -553,6 +556,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         qc = qload(q0);
         issue(q0, qc, q1);
     }
+    // block setup while the first round is in flight: the head of g and
+    // zeroed group histograms
+    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
+    for (int w = 0; w < LY::WARPS; ++w) {
+        double *h = reinterpret_cast<double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
+        for (int j = threadIdx.x; j < LY::NHIST * HS; j += blockDim.x) h[j] = 0.0;
+    }
+    __syncthreads();
+#ifdef SPFOM_DIAG_TIME
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     uint32_t phase = 0;
     for (; q0 >= 0; q0 = q1, q1 = q2, q2 = fnext(), phase ^= 1u) {
         const int64_t r = q0;
@@ -591,16 +605,31 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         const double z0 = sv.x;
         int idx[NE];
         double v[NE], om[NE], z[NE];
+        double gpre[EQ > 0 ? NE : 1];
         if constexpr (EQ > 0) {
-            // entry mapping: entry gl of quads qa, qa + 1, .. of the row
+            // entry mapping: entry gl of quads qa, qa + 1, .. of the row.  The
+            // ids first and the price gather right away (a2), so the L2 reads
+            // of the tail prices are in flight while v, omega and y are read
+            int pos[NE];
 #pragma unroll
             for (int t = 0; t < EQ; ++t) {
                 const int32_t q = qa + t;
-                const int p = 4 * (q < qb ? q - base : LY::QMAX) + gl;   // no quad: the inert zero quad
-                idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[p];
-                v[t] = reinterpret_cast<const double *>(slot + LY::OFF_V)[p];
-                om[t] = reinterpret_cast<const double *>(slot + LY::OFF_OM)[p];
-                z[t] = reinterpret_cast<const double *>(slot + LY::OFF_Y)[p];
+                pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + gl;   // no quad: the inert zero quad
+                idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[pos[t]];
+            }
+            uint32_t gh_s = ghead_s;
+            const double *gglob = S.g;
+            asm volatile("" : "+r"(gh_s), "+l"(gglob));
+#pragma unroll
+            for (int t = 0; t < EQ; ++t) {
+                const int j = idx[t];
+                gpre[t] = (j < HG) ? lds_f64(gh_s + 8u * (uint32_t)j) : __ldg(gglob + j);
+            }
+#pragma unroll
+            for (int t = 0; t < EQ; ++t) {
+                v[t] = reinterpret_cast<const double *>(slot + LY::OFF_V)[pos[t]];
+                om[t] = reinterpret_cast<const double *>(slot + LY::OFF_OM)[pos[t]];
+                z[t] = reinterpret_cast<const double *>(slot + LY::OFF_Y)[pos[t]];
             }
         } else
 #pragma unroll
@@ -634,7 +663,9 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
-            const double gj = (j < HG) ? lds_f64(gh_s + 8u * (uint32_t)j) : __ldg(gglob + j);
+            double gj;
+            if constexpr (EQ > 0) gj = gpre[e];
+            else gj = (j < HG) ? lds_f64(gh_s + 8u * (uint32_t)j) : __ldg(gglob + j);
             if constexpr (ARGMAX) z[e] = gj;             // theta = inf: keep g itself
             else z[e] = fma(S.theta, gj, z[e]);          // a3: z = y + theta g
         }
@@ -806,12 +837,16 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
     const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
     constexpr int CH = SPFOM_DYN_CH_MP;
     const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
-    auto grab = [&]() -> int32_t {
+    auto grab = [&]() -> unsigned long long {
         unsigned long long c = 0;
         if (lane == 0) c = atomicAdd(L.work, 1ull);
+        return c;
+    };
+    auto bcast = [&](unsigned long long c) -> int32_t {
         return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
     };
-    int32_t fpos = 0, fend = 0, fpend = 0;
+    int32_t fpos = 0, fend = 0;
+    unsigned long long fpend = 0;
     if constexpr (CH > 0) {
         fpend = grab();
     } else {
@@ -823,8 +858,9 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
     auto fnext = [&]() -> int32_t {
         if constexpr (CH > 0) {
             if (fpos >= fend) {
-                if (fpend >= nch) return -1;
-                fpos = fpend * CH;
+                const int32_t c = bcast(fpend);
+                if (c >= nch) return -1;
+                fpos = c * CH;
                 fend = min(fpos + CH, rounds);
                 fpend = grab();
             }
