@@ -206,6 +206,7 @@ struct spfom_handle {
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> qoff_h;               // device-order quad offsets [m + 1] (host copy)
+    bool bin_uniform[kNumBins] = {false};      // entry-mapped bin whose rows all have exactly E quads
     double *pin[2] = {nullptr, nullptr};       // pinned D2H staging ring (getters), allocated on first use
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
@@ -416,6 +417,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
                 SL.work = slot_ptr<unsigned long long>(h, O_WORK) + b;
+                SL.uni = h->bin_uniform[b] ? 1 : 0;
                 // several bins: concurrent persistent kernels on disjoint SM shares
                 // (forked streams; inside a graph they become parallel branches)
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
@@ -926,6 +928,10 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     if (bad_numeric) { h->err = "non-finite vt0"; return bail(SPFOM_EDATA); }
 
     h->qoff_h = qoff;
+    for (int b = 0; b < kNumBins; ++b) {
+        const int64_t k0 = h->bin_first[b], k1 = h->bin_first[b + 1];
+        h->bin_uniform[b] = kBins[b].E > 0 && k1 > k0 && (int64_t)qoff[k1] - qoff[k0] == (k1 - k0) * kBins[b].E;
+    }
     ptimer.mark("padded CSR (omp)");
     // ---- sampled block tables: per (iteration, bin) lists of device slots
     if (pl.sampled) {

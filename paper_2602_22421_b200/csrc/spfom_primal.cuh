@@ -416,6 +416,7 @@ struct StreamList {
     int32_t ghead;          // g staged in shared memory for products [0, ghead)
     int32_t hh;             // group histograms cover products [0, hh) (<= Layout::HH)
     unsigned long long *work;   // dynamic round chunks: counter zeroed before the launch
+    int32_t uni;            // entry mapping: every row of the bin has exactly EQ quads
 };
 
 template <int G, int Q, int EQ = 0>
@@ -611,12 +612,20 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             // ids first and the price gather right away (a2), so the L2 reads
             // of the tail prices are in flight while v, omega and y are read
             int pos[NE];
+            if (L.uni && left >= GPW) {
+                // uniform rows, full round: group g's row is quads [EQ g, EQ g + EQ) of
+                // the slot -- constant offsets, no per-entry bounds test
 #pragma unroll
-            for (int t = 0; t < EQ; ++t) {
-                const int32_t q = qa + t;
-                pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + gl;   // no quad: the inert zero quad
-                idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[pos[t]];
+                for (int t = 0; t < EQ; ++t) pos[t] = 4 * (EQ * gidx + t) + gl;
+            } else {
+#pragma unroll
+                for (int t = 0; t < EQ; ++t) {
+                    const int32_t q = qa + t;
+                    pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + gl;   // no quad: the inert zero quad
+                }
             }
+#pragma unroll
+            for (int t = 0; t < EQ; ++t) idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[pos[t]];
             uint32_t gh_s = ghead_s;
             const double *gglob = S.g;
             asm volatile("" : "+r"(gh_s), "+l"(gglob));
@@ -678,10 +687,15 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 
         // ---- write back (y, segment state), a5 usage scatter
         if constexpr (EQ > 0) {
+            // the group's 4 lanes write each quad's 32-B sector
+            double *yp = S.y + 4 * (int64_t)qa + gl;
+            if (L.uni && left >= GPW) {
 #pragma unroll
-            for (int t = 0; t < EQ; ++t) {
-                const int32_t q = qa + t;
-                if (q < qb) S.y[4 * (int64_t)q + gl] = yv[t];   // the group's 4 lanes write the quad's 32-B sector
+                for (int t = 0; t < EQ; ++t) yp[4 * t] = yv[t];
+            } else {
+#pragma unroll
+                for (int t = 0; t < EQ; ++t)
+                    if (qa + t < qb) yp[4 * t] = yv[t];
             }
         } else
 #pragma unroll

@@ -105,13 +105,16 @@ def test_ragged_lengths_cross_every_bin_and_pad():
     _assert_ok(worst)
 
 
-@pytest.mark.parametrize("preset", ["converge", "paper"])
-def test_entry_mapped_bin_lockstep(preset):
-    """Rows of 49..52 entries (13 quads, the k = 50 configs) run on the full-
-    sweep stream kernel's entry mapping (bin E = 13: 4 lanes x 13 entries,
-    DESIGN.md §7).  24000 segments give every warp >= 2 rounds, so the
-    throughput mapping runs, not the wide latency one; pads of width 0..3."""
-    inst = generate("huge", m=24000, N=3000, k=(49, 52))
+@pytest.mark.parametrize("preset,k", [("converge", (49, 52)), ("paper", (49, 52)), ("converge", (33, 52)),
+                                      ("converge", 50)])
+def test_entry_mapped_bin_lockstep(preset, k):
+    """Rows of 33..52 entries (9..13 quads; the k = 50 configs have 13) run on
+    the full-sweep stream kernel's entry mapping (bin E = 13: 4 lanes x 13
+    entries).  k in 49..52 or k = 50: every row has exactly 13
+    quads (the uniform-row fast path; the last round of the bin is partial);
+    33..52: ragged rows (per-entry bounds).  24000 segments give every warp >= 2
+    rounds, so the throughput mapping runs, not the wide latency one."""
+    inst = generate("huge", m=24000 + 5, N=3000, k=k)
     p = _params(exec_mode=1) if preset == "converge" else _paper(mu=0.5, exec_mode=1)
     worst, gpu, _ = lockstep(inst, p, 30)
     gpu.close()
