@@ -1067,13 +1067,18 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
     }
     // several active bins: concurrent launches on SM shares proportional to each bin's work
-    // (full sweep: padded entries; sampled: the largest per-iteration count x capacity)
+    // (full sweep: padded entries x the bin's measured cost per entry; sampled: the largest
+    // per-iteration count x capacity)
     if (!h->small) {
         int64_t wtot = 0, w[kNumBins] = {0};
         for (int b = 0; b < kNumBins; ++b) {
             const int64_t cnt = pl.sampled ? h->pl.bin_count[b] : (h->bin_first[b + 1] - h->bin_first[b]);
+            // B200, medium config: an SM streams ~20 KB/us of a 4-lane bin, 16.0 of a
+            // 16-lane and 13.6 of a 32-lane one (wider groups: more butterfly steps and
+            // fewer segments per warp round), so wide bins get proportionally more SMs
+            const double cost = kBins[b].G >= 32 ? 1.5 : (kBins[b].G >= 16 ? 1.28 : 1.0);
             w[b] = pl.sampled ? cnt * bin_cap(kBins[b])
-                              : (int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt;
+                              : (int64_t)(cost * (double)((int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt));
             if (cnt > 0) h->nbins_active += 1;
             wtot += w[b];
         }
