@@ -162,9 +162,12 @@ typedef struct {
     int64_t refresh_every;
 } spfom_params;
 
-/* Distribution: world == 1 => single GPU (nccl_id ignored).  Otherwise
- * nccl_id points at the 128-byte ncclUniqueId produced on rank 0 by
- * spfom_nccl_unique_id() and broadcast by the caller (torch.distributed). */
+/* Distribution: nccl_id points at the 128-byte
+ * ncclUniqueId produced on rank 0 by spfom_nccl_unique_id() and broadcast by
+ * the caller (torch.distributed).  world > 1 needs it.  world == 1 with
+ * nccl_id == NULL (or no spfom_dist at all) => single GPU; world == 1 with an
+ * id runs the multi-rank code path (NCCL allreduce of the usage, k_fold) on
+ * one GPU with identical results -- a way to exercise it without peers. */
 typedef struct {
     int32_t rank;
     int32_t world;

@@ -242,7 +242,7 @@ template <typename T>
 T *slot_ptr(spfom_handle *h, int s) { return reinterpret_cast<T *>(h->ws + h->pl.off[s]); }
 
 spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, int dtype, int op) {
-    if (h->world <= 1) {
+    if (!h->comm) {
         if (src != dst) CUDA_TRY(h, cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, h->stream));
         return SPFOM_OK;
     }
@@ -464,7 +464,7 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
         full_mode = 1;
         ++nl;
     }
-    if (h->world > 1 && S.spread_n > 0) {
+    if (h->comm && S.spread_n > 0) {
         // fold the spread copies into acc before the cross-rank sum
         k_fold<<<std::max<int64_t>(1, (S.spread_n + kThreads - 1) / kThreads), kThreads, 0, h->stream>>>(S);
         ++nl;
@@ -733,8 +733,10 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         return s;
     };
 
-    if (dist && dist->world > 1) {
-        if (!nccl().ok) { h->err = "world > 1 but libnccl.so.2 not loadable"; return bail(SPFOM_ENCCL); }
+    // distributed mode: world > 1, or world == 1 with an NCCL id (the multi-rank
+    // code path -- NCCL allreduce, k_fold -- on one GPU; tests use it)
+    if (dist && (dist->world > 1 || dist->nccl_id)) {
+        if (!nccl().ok) { h->err = "distributed mode but libnccl.so.2 not loadable"; return bail(SPFOM_ENCCL); }
         if (!dist->nccl_id || dist->rank < 0 || dist->rank >= dist->world) { h->err = "bad spfom_dist"; return bail(SPFOM_EINVAL); }
         h->rank = dist->rank;
         h->world = dist->world;
@@ -755,7 +757,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
 #pragma omp critical
         for (int64_t j = 0; j <= N; ++j) counts[j] += loc[j];
     }
-    if (h->world > 1) {
+    if (h->comm) {
         int64_t *dcounts = slot_ptr<int64_t>(h, O_COUNTS);
         if (cudaMemcpyAsync(dcounts, counts.data(), N * 8, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) { h->err = "H2D counts"; return bail(SPFOM_ECUDA); }
         if (allreduce(h, dcounts, dcounts, N, kNcclInt64, kNcclSum) != SPFOM_OK) return bail(SPFOM_ENCCL);
@@ -1017,7 +1019,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.spread = S.s + S.spread_off;
     S.spread_n = (int32_t)spread_range(N);
     S.spread_c = kSpreadCopies;
-    S.fold_in_dual = h->world > 1 ? 0 : 1;
+    S.fold_in_dual = h->comm ? 0 : 1;
     S.s_prev = slot_ptr<double>(h, O_SCUR);
     S.etabar = pl.averaging ? slot_ptr<double>(h, O_ETABAR) : nullptr;
     S.counters = slot_ptr<unsigned long long>(h, O_COUNTERS);
@@ -1037,7 +1039,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         int64_t max_rq = 0;
         for (int64_t k = 0; k < m; ++k) max_rq = std::max<int64_t>(max_rq, qoff[k + 1] - qoff[k]);
         const int64_t per_iter = pl.sampled ? p->block_size : m;
-        const bool eligible = h->world == 1 && T == 1 && h->L == 0 && !pl.averaging && !(pl.sampled && p->refresh_every > 0) &&
+        const bool eligible = !h->comm && T == 1 && h->L == 0 && !pl.averaging && !(pl.sampled && p->refresh_every > 0) &&
                               max_rq <= 256 && per_iter <= 4096;
         if (p->exec_mode == 2 && !eligible) {
             h->err = "exec_mode 2 needs world == 1, T == 1, no averaging/refresh, rows <= 1024 entries, <= 4096 segments per iteration";
@@ -1331,7 +1333,7 @@ spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     for (size_t b = 0; b < hr.size() / 8; ++b)      // bundles: the capacity rows are resources
         for (int k = 0; k < 8; ++k)
             pr[k] = (k == 2 || k == 3 || k == 7) ? std::max(pr[k], hr[8 * b + k]) : pr[k] + hr[8 * b + k];
-    if (h->world > 1) {
+    if (h->comm) {
         double buf[4] = {dseg, agg[0], agg[1], agg[2]};
         CUDA_TRY(h, cudaMemcpyAsync(red, buf, 32, cudaMemcpyHostToDevice, h->stream));
         if ((st = allreduce(h, red, red, 1, kNcclFloat64, kNcclSum)) != SPFOM_OK) return st;
@@ -1440,7 +1442,7 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
     }
     out->primal_launches_per_iteration = np;
     // primal launches + K3 (+ k_average + k_tick with averaging) (+ k_fold when world > 1)
-    out->launches_per_iteration = np + 1 + (h->pl.averaging ? 2 : 0) + (h->world > 1 && h->S.spread_n > 0 ? 1 : 0) +
+    out->launches_per_iteration = np + 1 + (h->pl.averaging ? 2 : 0) + (h->comm && h->S.spread_n > 0 ? 1 : 0) +
                                   (h->L > 0 ? 2 : 0);
     return SPFOM_OK;
 }

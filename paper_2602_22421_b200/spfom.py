@@ -251,7 +251,7 @@ class Solver:
         aligned = (base + 255) & ~255
         self._id = None
         dist = None
-        if world > 1:
+        if world > 1 or nccl_id is not None:      # world == 1 + id: the multi-rank path on one GPU
             if nccl_id is None or len(nccl_id) != 128:
                 raise SpfomError(1, "world > 1 needs the 128-byte nccl_id from rank 0")
             self._id = C.create_string_buffer(nccl_id, 128)

@@ -466,3 +466,35 @@ def test_feature_combinations_lockstep(combo):
         assert rel_inf(eb, cpu.etabar, rmax) <= TOL_ITER
     gpu.close()
     _assert_ok(worst)
+
+
+@pytest.mark.parametrize("name,kw", [("medium", dict(m=30000, N=4000, k=(20, 200))),
+                                     ("multi", dict(m=3000, N=800, k=50, T=3))])
+def test_nccl_path_single_rank(name, kw):
+    """The multi-rank code path (ncclCommInitRank from a unique id, k_fold of the
+    spread copies, ncclAllReduce of the usage inside the CUDA graph, global
+    column counts by allreduce) run with world == 1 on this GPU: iterates equal
+    to the single-GPU path up to the order of the fp64 reductions (K1's global
+    RED order is not fixed, so two runs are not bitwise equal) and within
+    1e-10 of the oracle."""
+    from paper_2602_22421_b200 import Params, Solver, nccl_unique_id
+    inst = generate(name, **kw)
+    p = Params.converge(exec_mode=1)
+    a = Solver(inst, p)
+    b = Solver(inst, p, rank=0, world=1, nccl_id=nccl_unique_id())
+    assert b.info()["launches_per_iteration"] == a.info()["launches_per_iteration"] + 1   # + k_fold
+    cpu = oracle.OracleSolver(inst, **oracle_kwargs(p))
+    for _ in range(20):
+        a.step(1)
+        b.step(1)
+        cpu.step()
+    ya, y0a = a.primal()
+    yb, y0b = b.primal()
+    lam, rmax = float(inst.arrival.max()), float(inst.price.max())
+    assert rel_inf(yb, ya, lam) <= 1e-12 and rel_inf(y0b, y0a, lam) <= 1e-12
+    assert rel_inf(b.duals(), a.duals(), rmax) <= 1e-12
+    assert rel_inf(yb, cpu.y, lam) <= TOL_ITER and rel_inf(b.duals(), cpu.eta, rmax) <= TOL_ITER
+    ra, rb = a.residuals(), b.residuals()
+    assert abs(ra["primal_obj"] - rb["primal_obj"]) <= 1e-12 * abs(ra["primal_obj"])
+    a.close()
+    b.close()
