@@ -1,6 +1,7 @@
 """Summarise ncu outputs into profiles/ (run here, no GPU needed).
 
   python profiles/summarize.py ROUND gpurun_out/prof_k1.ncu-rep gpurun_out/launches.csv
+  python profiles/summarize.py --late ROUND gpurun_out/prof_late.ncu-rep paper_2602_22421_b200/libspfom.so
 
 writes profiles/<ROUND>_k1_full.txt (key metrics, stall reasons, instruction
 mix), profiles/<ROUND>_launches.csv (the per-launch list) and updates
@@ -86,7 +87,81 @@ def write_launch_summary(rnd, path):
     print("\n".join(lines))
 
 
+def write_late(rnd, rep, so):
+    """Steady-state capture (exp/prof_late.sh, iteration ~1500): key metrics,
+    stall reasons and the source lines that take the most stall samples, from
+    the SASS source page mapped to CUDA lines through `nvdisasm -g` of the
+    library that ran (`so`)."""
+    import tempfile
+    mets = raw_metrics(rep)
+    stalls, mix, _ = sass_profile(rep)
+    kname = mets[0]["kernel"]
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
+    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    mangled = None
+    for ln in dis.splitlines():
+        if ln.startswith("//----") and "k_primal_stream" in ln and "Lb0ELi13E" in ln:
+            mangled = ln.split(".text.")[1].split()[0]
+            break
+    off2loc, cur, inside = {}, None, False
+    for ln in dis.splitlines():
+        if ln.startswith("//----"):
+            inside = mangled is not None and mangled in ln
+            continue
+        if not inside:
+            continue
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
+        if m:
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            continue
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
+        if m:
+            off2loc[int(m.group(1), 16)] = cur
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, data = rows[1], rows[2:]
+    iI, iS = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
+    agg = collections.defaultdict(lambda: [0.0, 0.0])
+    base = None
+    for r in data:
+        if not r or not r[0].startswith("0x"):
+            continue
+        a = int(r[0], 16)
+        base = a if base is None else base
+        loc = off2loc.get(a - base)
+        agg[loc][0] += float(r[iI] or 0)
+        agg[loc][1] += float(r[iS] or 0)
+    ti = sum(v[0] for v in agg.values()) or 1.0
+    ts = sum(v[1] for v in agg.values()) or 1.0
+    src = {}
+    lines = [f"ncu --set full of one K1 launch in the steady state ({os.path.basename(rep)}), round {rnd}", "",
+             f"kernel: {kname}"]
+    for k in KEYS:
+        if k in mets[0]:
+            lines.append(f"  {k:62s} {mets[0][k][0]} {mets[0][k][1]}")
+    lines += ["", "stall reasons (% of samples): " + ", ".join(f"{k} {v:.1f}" for k, v in
+                                                            sorted(stalls.items(), key=lambda x: -x[1])[:10]),
+              "", "source lines by stall samples (% samples, % instructions):"]
+    for loc, (n, smp) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
+        text = ""
+        if loc:
+            if loc[0] not in src:
+                pth = os.path.join(os.path.dirname(HERE), "paper_2602_22421_b200", "csrc", loc[0])
+                src[loc[0]] = open(pth).read().splitlines() if os.path.exists(pth) else []
+            if loc[1] - 1 < len(src[loc[0]]):
+                text = src[loc[0]][loc[1] - 1].strip()[:80]
+        lines.append(f"  {smp / ts * 100:5.1f}% {n / ti * 100:5.1f}%  {loc[0] if loc else '?'}:{loc[1] if loc else ''}  {text}")
+    open(os.path.join(HERE, f"{rnd}_k1_late.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 def main():
+    if sys.argv[1] == "--late":
+        write_late(sys.argv[2], sys.argv[3], sys.argv[4])
+        return
     rnd, rep = sys.argv[1], sys.argv[2]
     launches = sys.argv[3] if len(sys.argv) > 3 else None
     mets = raw_metrics(rep)
