@@ -156,6 +156,21 @@ __device__ __forceinline__ double lds_f64_v(uint32_t a) {
 __device__ __forceinline__ void sts_f64(uint32_t a, double x) {
     asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(x) : "memory");
 }
+// Lane 0 claims the next work chunk (atomic add on a global counter); the
+// result register is written by the predicated atomic itself and first read
+// when the warp moves to that chunk, so nothing waits on the atomic's latency
+// (a C-level `if (lane == 0) c = atomicAdd(..)` gets a merge right after it).
+// The increment is written as lane + 1 (= 1 on lane 0): with a warp-uniform
+// operand ptxas rewrites the atomic into its warp-aggregated form, whose
+// shuffle of the result right after the atomic would wait for it.
+__device__ __forceinline__ unsigned long long claim_chunk(unsigned long long *ctr, int lane) {
+    unsigned long long c = 0;
+    const unsigned long long inc = (unsigned long long)(lane + 1);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, 0;\n\t@p atom.global.add.u64 %0, [%2], %3;\n\t}"
+                 : "+l"(c) : "r"(lane), "l"(ctr), "l"(inc) : "memory");
+    return c;
+}
+
 // fp64 reduction into global memory under a predicate, without a branch
 __device__ __forceinline__ void red_add_if(double *p, double v, bool pred) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p red.global.add.f64 [%0], %1;\n\t}"

@@ -483,11 +483,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     // the claimed chunk id stays in lane 0's register until the warp moves to
     // that chunk (the broadcast is the first use: the atomic's latency is
     // hidden behind the current chunk's rounds)
-    auto grab = [&]() -> unsigned long long {
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(L.work, 1ull);
-        return c;
-    };
+    auto grab = [&]() -> unsigned long long { return claim_chunk(L.work, lane); };
     auto bcast = [&](unsigned long long c) -> int32_t {
         return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
     };
@@ -851,11 +847,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
     const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
     constexpr int CH = SPFOM_DYN_CH_MP;
     const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
-    auto grab = [&]() -> unsigned long long {
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(L.work, 1ull);
-        return c;
-    };
+    auto grab = [&]() -> unsigned long long { return claim_chunk(L.work, lane); };
     auto bcast = [&](unsigned long long c) -> int32_t {
         return __shfl_sync(0xffffffffu, (int32_t)(c < 0x7fffffffull ? c : 0x7fffffffull), 0);
     };
