@@ -295,24 +295,25 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
 }
 
 // Multi-period shared structure: units = rounds x T over one persistent block per SM.
-template <int G, int Q, bool ARGMAX>
+template <int G, int Q, bool ARGMAX, int EQ = 0>
 void launch_mp(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
+    using LY = MPLayout<G, Q, EQ>;
     static int hg_cap = -1;
-    constexpr size_t fixed = mp_smem_fixed<G, Q>();
+    constexpr size_t fixed = mp_smem_fixed<G, Q, EQ>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
-        cudaFuncSetAttribute(k_primal_mp<G, Q, ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_primal_mp<G, Q, ARGMAX, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(fixed + (size_t)hg_cap * 8));
     }
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
     L.hh = 0;
-    constexpr int W = MPLayout<G, Q>::WARPS;
-    const int64_t rounds = (L.count + MPLayout<G, Q>::GPW - 1) / MPLayout<G, Q>::GPW;
+    constexpr int W = LY::WARPS;
+    const int64_t rounds = (L.count + LY::GPW - 1) / LY::GPW;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
-    k_primal_mp<G, Q, ARGMAX><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+    k_primal_mp<G, Q, ARGMAX, EQ><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
 void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
@@ -320,8 +321,8 @@ void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int
 #define CASE(B, G, Q, E)                                                                   \
     case B:                                                                                \
         if constexpr (Q <= 4) {                                                            \
-            if (argmax) launch_mp<G, Q, true>(S, L, sms, st);                              \
-            else launch_mp<G, Q, false>(S, L, sms, st);                                    \
+            if (argmax) launch_mp<G, Q, true, E>(S, L, sms, st);                           \
+            else launch_mp<G, Q, false, E>(S, L, sms, st);                                 \
         }                                                                                  \
         break;
         SPFOM_BINS(CASE)

@@ -772,12 +772,13 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 // than in the stacked layout.  Two TMA slots per warp: the structure of round
 // r + 1 and the per-period data of the next unit are fetched while the current
 // unit computes.
-template <int G, int Q>
+template <int G, int Q, int EQ = 0>
 struct MPLayout {
-    static constexpr int WARPS = (4 * Q >= 16) ? SPFOM_STREAM_WARPS_WIDE : SPFOM_STREAM_WARPS;
+    static_assert(EQ == 0 || G == 4, "entry mapping: 4 lanes per segment");
+    static constexpr int WARPS = (EQ > 0 || 4 * Q >= 16) ? SPFOM_STREAM_WARPS_WIDE : SPFOM_STREAM_WARPS;
     static constexpr int GPW = 32 / G;
-    static constexpr int NE = 4 * Q;
-    static constexpr int QMAX = GPW * G * Q;
+    static constexpr int NE = EQ ? EQ : 4 * Q;          // entries per lane (EQ: entry mapping, as K1 stream)
+    static constexpr int QMAX = GPW * (EQ ? EQ : G * Q);
     static constexpr int QW = ((GPW + 8) + 3) & ~3;
     // structure slot (index QMAX of each quad array: inert zero quad)
     static constexpr uint32_t S_QW = 0;
@@ -796,14 +797,14 @@ struct MPLayout {
     static constexpr uint32_t PER_WARP = YS + 256u * NE;
 };
 
-template <int G, int Q>
+template <int G, int Q, int EQ = 0>
 __host__ __device__ constexpr size_t mp_smem_fixed() {
-    return (size_t)MPLayout<G, Q>::WARPS * MPLayout<G, Q>::PER_WARP + 256;   // + 2 mbarriers per warp
+    return (size_t)MPLayout<G, Q, EQ>::WARPS * MPLayout<G, Q, EQ>::PER_WARP + 256;   // + 2 mbarriers per warp
 }
 
-template <int G, int Q, bool ARGMAX>
-__global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(DevState S, StreamList L) {
-    using LY = MPLayout<G, Q>;
+template <int G, int Q, bool ARGMAX, int EQ = 0>
+__global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp(DevState S, StreamList L) {
+    using LY = MPLayout<G, Q, EQ>;
     constexpr int NE = LY::NE;
     constexpr int GPW = LY::GPW;
     static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
@@ -821,7 +822,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
     unsigned char *ws = smem + (size_t)warp * LY::PER_WARP;
     uint64_t *barS = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + 2 * warp;
     uint64_t *barP = barS + 1;
-    double *ghead = reinterpret_cast<double *>(smem + mp_smem_fixed<G, Q>());
+    double *ghead = reinterpret_cast<double *>(smem + mp_smem_fixed<G, Q, EQ>());
     const uint32_t ghead_s = smem_u32(ghead);
     const uint32_t gt_s = smem_u32(ws + LY::GT) + 8u * lane, ys_s = smem_u32(ws + LY::YS) + 8u * lane;
     const int spread_n = S.spread_n;
@@ -938,6 +939,17 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
         const int32_t base = __shfl_sync(0xffffffffu, qc, 0);
         const int32_t qa = __shfl_sync(0xffffffffu, qc, gidx);
         const int32_t qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
+        int epos[EQ > 0 ? NE : 1];                     // entry mapping: slot entry of each of this lane's entries
+        if constexpr (EQ > 0) {
+#pragma unroll
+            for (int t = 0; t < EQ; ++t) {
+                const int32_t q = qa + t;
+                epos[t] = 4 * (q < qb ? q - base : LY::QMAX) + gl;
+                idx[t] = reinterpret_cast<const int *>(ws + LY::S_IDS)[epos[t]];
+                v[t] = reinterpret_cast<const double *>(ws + LY::S_V)[epos[t]];
+                om[t] = reinterpret_cast<const double *>(ws + LY::S_OM)[epos[t]];
+            }
+        } else
 #pragma unroll
         for (int tq = 0; tq < Q; ++tq) {
             const int32_t q = qa + gl + G * tq;
@@ -975,6 +987,10 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
                 vt0 = sc.y;
             }
             double z[NE];
+            if constexpr (EQ > 0) {
+#pragma unroll
+                for (int t = 0; t < EQ; ++t) z[t] = reinterpret_cast<const double *>(ws + LY::P_Y)[epos[t]];
+            } else
 #pragma unroll
             for (int tq = 0; tq < Q; ++tq) {
                 const int32_t q = qa + gl + G * tq;
@@ -998,6 +1014,11 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q>::WARPS, 1) k_primal_mp(Dev
             else project_group<G, NE>(z, v, om, sv.x, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
 
             // ---- write back y_t and the segment state; accumulate sum_t y
+            if constexpr (EQ > 0) {
+#pragma unroll
+                for (int tt = 0; tt < EQ; ++tt)
+                    if (qa + tt < qb) S.y[4 * (t * nqb + qa + tt) + gl] = yv[tt];
+            } else
 #pragma unroll
             for (int tq = 0; tq < Q; ++tq) {
                 const int32_t q = qa + gl + G * tq;
