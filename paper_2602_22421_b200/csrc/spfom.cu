@@ -202,7 +202,7 @@ struct spfom_handle {
     int64_t L = 0;                                                  // resources (bundles / NRM), 0 = none
     std::vector<int32_t> bptr_h, bres_h;                            // relabelled bundle CSR (set_state)
     std::vector<int32_t> new2old, old2new;     // products
-    std::unique_ptr<int64_t[]> pos_map;        // original entry -> padded entry [nnz] (no zero-fill)
+    std::unique_ptr<int32_t[]> pos_map;        // original entry -> padded entry [nnz] (no zero-fill; < 2^31 by validation)
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> qoff_h;               // device-order quad offsets [m + 1] (host copy)
@@ -578,6 +578,8 @@ static spfom_status validate(const spfom_instance *in, const spfom_params *p) {
     const int64_t T = std::max<int64_t>(1, in->num_periods);
     if (T > 1 && p && p->blocks) return fail(nullptr, SPFOM_EINVAL, "sampled blocks are not supported with num_periods > 1");
     if (N >= INT32_MAX) return fail(nullptr, SPFOM_EDATA, "instance: num_products too large");
+    if (in->nnz + 3 * m >= INT32_MAX)   // padded entries index int32 device offsets
+        return fail(nullptr, SPFOM_EDATA, "instance: too many entries for one GPU (shard it over more ranks)");
     // per-segment rules: a parallel scan finds the first offending segment, the
     // serial loop below (from there) reports it
     int64_t first_bad = m;
@@ -852,7 +854,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     const int64_t T = h->T;
     std::vector<double2> segc(std::max<int64_t>(T * m, 1));
     std::vector<double4> segv(std::max<int64_t>(T * m, 1));
-    h->pos_map.reset(new int64_t[std::max<int64_t>(in->nnz, 1)]);
+    h->pos_map.reset(new int32_t[std::max<int64_t>(in->nnz, 1)]);
     h->seg_off.assign(in->seg_ptr, in->seg_ptr + m + 1);
     bool bad_numeric = false;
     // The padded arrays (ids, v, omega) are built chunk by chunk of device
@@ -907,7 +909,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
                 om[base - pbase + q] = w / v;
                 vt0 += w;
                 svt += v - w;
-                h->pos_map[e] = base + q;
+                h->pos_map[e] = (int32_t)(base + q);
             }
             for (int64_t t = 0; t < T; ++t) {
                 const double lam = in->arrival[t * m + i];
@@ -1238,7 +1240,7 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
                 k0 = k1;
             }
         }
-        const int64_t *pm = h->pos_map.get();
+        const int32_t *pm = h->pos_map.get();
         const double *pin_of[2] = {h->pin[0], h->pin[1]};
         auto issue = [&](size_t c) -> spfom_status {
             const Chunk &ch = chunks[c];
