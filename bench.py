@@ -24,6 +24,13 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Eager CUDA module loading (read at CUDA initialisation, so before torch
+# touches the GPU).  Measured on B200: with the default lazy loading the
+# primal kernel K1 runs ~15% slower in a live loop than the same launch under
+# ncu or with eager loading (huge: 0.49 vs 0.42 ms; bench 1930 vs 2111 it/s);
+# DESIGN.md §9.  An explicit setting in the environment wins.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 METRIC = "SPFOM iterations/s (fp64, full sweep)"
 UNIT = "iterations/s"
 BYTES_PER_NNZ = 36        # prod_idx 4 + v 8 + omega 8 + y read 8 + y write 8
@@ -220,7 +227,8 @@ def workload_config(inst, world):
             "parallelism": f"segments sharded over {world} GPU(s) by nnz; NCCL allreduce of s each iteration"
             if world > 1 else "1 GPU",
             "l2": "no flush: per-iteration working set 1.8 GB >> 126 MB L2" if inst.nnz > 10_000_000 else
-            "working set fits L2 (no flush)"}
+            "working set fits L2 (no flush)",
+            "cuda_module_loading": os.environ.get("CUDA_MODULE_LOADING", "LAZY")}
 
 
 # --------------------------------------------------------------------- time to gap
