@@ -512,11 +512,15 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         return fpos++;
     };
 
+    // uniform entry-mapped bin: every row has EQ quads, so a segment's quad
+    // offset is arithmetic (no qoff reads, no window copy per round)
+    const bool uni = EQ > 0 && L.uni;
+    const int32_t qbase = uni ? S.qoff[L.first] : 0;
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
         int64_t k = GPW * r + (lane < GPW ? lane : GPW);
         k = k < L.count ? k : L.count;
-        return S.qoff[L.first + k];
+        return uni ? qbase + (int32_t)(EQ * k) : S.qoff[L.first + k];
     };
     // lane 0 issues the bulk copies of round r (q: this lane's qoff of round r):
     // segment state, quads, and (rw >= 0) the 16-B aligned qoff window that
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
         const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;        // window of round rw
-        const uint32_t wbytes = rw >= 0 ? 4u * LY::QW : 0u;
+        const uint32_t wbytes = (rw >= 0 && !uni) ? 4u * LY::QW : 0u;
         // one elected lane, straight-line: the copies take uniform operands
         if (lane == 0) {
             mbar_arrive_expect_tx(bar, 48u * n + 112u * nq + wbytes);
@@ -581,7 +585,8 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             const int64_t s1 = L.first + GPW * (int64_t)q1;
             int64_t k = GPW * (int64_t)q1 + (lane < GPW ? lane : GPW);
             k = k < L.count ? k : L.count;
-            qn = reinterpret_cast<const int32_t *>(slot + LY::OFF_QW)[L.first + k - (s1 & ~(int64_t)3)];
+            qn = uni ? qbase + (int32_t)(EQ * k)
+                     : reinterpret_cast<const int32_t *>(slot + LY::OFF_QW)[L.first + k - (s1 & ~(int64_t)3)];
         }
         const int32_t base = __shfl_sync(0xffffffffu, qc, 0);
         const int32_t qa = __shfl_sync(0xffffffffu, qc, gidx);
