@@ -199,7 +199,12 @@ class Solver:
     def __init__(self, inst, params: Optional[Params] = None, *, device=None, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  segment_offset: int = 0, num_segments_global: Optional[int] = None,
-                 shared_periods: bool = True):
+                 shared_periods: bool = True, workspace_offset_bytes: int = 0):
+        """workspace_offset_bytes > 0: a device allocation of that size is made
+        (and kept for the solver's lifetime) before the workspace, which then
+        lands above it -- measured on B200, a workspace in the low part of
+        device memory makes the primal kernel 0-15% slower, run to run
+        (DESIGN.md §9); bench.py uses 32 GiB."""
         import torch  # device memory and streams only
 
         L = load_library()
@@ -246,6 +251,8 @@ class Solver:
         with torch.cuda.device(self.device):
             # a dedicated stream: the legacy default stream cannot be captured into a CUDA graph
             self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+            self._placement_pad = (torch.empty(int(workspace_offset_bytes), dtype=torch.uint8, device=self.device)
+                                   if workspace_offset_bytes > 0 else None)
             self.workspace = torch.empty(max(int(nbytes.value), 256) + 256, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
@@ -347,6 +354,7 @@ class Solver:
         if getattr(self, "_h", None):
             load_library().spfom_destroy(self._h)
             self._h = None
+        self._placement_pad = None
 
     def __del__(self):
         try:
