@@ -94,6 +94,12 @@ typedef enum {
  *                averages) are per resource (length L); prices g_j = r_j -
  *                sum_{l in B_j} eta_l; tau_l = tau / n_l with n_l = sum_{j : l in B_j}
  *                n_j (tau_mode 1, reading c17).
+ *   on_device    0: every array above is host memory.  1: every array is device
+ *                memory readable from the current device (e.g. torch tensors):
+ *                spfom_workspace_bytes / spfom_create stage them to host memory
+ *                first (the layout build is a host pass) and keep no pointer;
+ *                unreadable pointers => SPFOM_EINVAL.  (SPEC S:L31-37 data model;
+ *                SURVEY §8(b) `on_device`.)
  * Violations are reported as SPFOM_EDATA.
  */
 typedef struct {
@@ -115,6 +121,7 @@ typedef struct {
     const int64_t *bundle_ptr;
     const int32_t *bundle_res;
     const double *resource_capacity;
+    int64_t on_device;
 } spfom_instance;
 
 /*
@@ -226,7 +233,15 @@ spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double
 spfom_status spfom_objective(spfom_handle *h, double *obj);       /* r^T (A y), fresh */
 spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out);
 
-/* Overwrite the iterate (checkpoint / resume): original orders, like the getters. */
+/* Overwrite the iterate (checkpoint / resume): original orders, like the getters.
+ * Any argument may be NULL (that part of the state is kept).  s_prev is the
+ * usage A y of the iterate (sampled mode: the running stale-inclusive usage the
+ * next dual step adds its delta to): when y is given without s_prev, the
+ * library recomputes s_prev = A y on the device (cross-rank sum when world > 1),
+ * so the next dual step is consistent with the restored y.  The projection's
+ * warm-start multipliers are kept (they only change the Newton starting point,
+ * not the result), and so are the iteration counter and, with averaging, the
+ * running averages (set_state restores the iterate, not the averages). */
 spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0, const double *eta,
                              const double *s_prev);
 

@@ -98,6 +98,37 @@ int bin_of(int64_t nq) {
 
 constexpr int kResidBlocks = 592;   // 4 x 148 SMs
 
+// Per-device launch facts (opt-in shared memory set on the kernel, occupancy):
+// cudaFuncSetAttribute applies to the current device's context only, so a
+// process driving several GPUs needs one entry per device.
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+    int v[kMaxDevices];
+    PerDevice() { for (int &x : v) x = -1; }
+    // the slot of the current device (devices past kMaxDevices share a
+    // sentinel that is never cached: the caller re-queries every time)
+    int *slot() {
+        static thread_local int scratch;
+        int d = 0;
+        cudaGetDevice(&d);
+        if (d >= 0 && d < kMaxDevices) return &v[d];
+        scratch = -1;
+        return &scratch;
+    }
+};
+
+// Makes the handle's device current for the duration of an entry point.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Plan {
@@ -215,6 +246,7 @@ struct spfom_handle {
     cudaGraphExec_t graph_primal = nullptr, graph_rest = nullptr, graph_rest_refresh = nullptr;   // split (timed) form
     std::string err;
     int sm_count = 148;
+    int device = 0;                            // every entry point runs with this device current
     bool own_stream = false;
     // full sweep with several non-empty bins: one side stream per bin, SM share per bin
     int nbins_active = 0;
@@ -256,9 +288,10 @@ spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, in
 // segments to amortise its flush (H REDs per block).
 template <int G, int Q, bool ARGMAX, bool SAMPLED>
 void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count, cudaStream_t st) {
-    static int resident = 0;
+    static PerDevice cache;
+    int &resident = *cache.slot();
     constexpr size_t smem = sizeof(ListSmem<Q, G>);
-    if (resident == 0) {
+    if (resident < 0) {
         cudaFuncSetAttribute(k_primal<G, Q, ARGMAX, SAMPLED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_primal<G, Q, ARGMAX, SAMPLED>, kPrimalThreads, smem);
         resident = std::max(resident, 1);
@@ -276,7 +309,8 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
 template <int G, int Q, bool ARGMAX, int EQ = 0>
 void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
     using LY = StreamLayout<G, Q, EQ>;
-    static int hg_cap = -1;
+    static PerDevice cache;
+    int &hg_cap = *cache.slot();
     constexpr size_t fixed = stream_smem_fixed<G, Q, EQ>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
@@ -298,7 +332,8 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
 template <int G, int Q, bool ARGMAX, int EQ = 0>
 void launch_mp(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
     using LY = MPLayout<G, Q, EQ>;
-    static int hg_cap = -1;
+    static PerDevice cache;
+    int &hg_cap = *cache.slot();
     constexpr size_t fixed = mp_smem_fixed<G, Q, EQ>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
@@ -513,6 +548,53 @@ spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, in
     if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     return SPFOM_OK;
 }
+
+// ------------------------------------------------------------------ device-resident instances
+// spfom_instance.on_device = 1: the arrays are device pointers (e.g. torch
+// tensors); the layout build is a host pass, so they are staged to host
+// memory first and the rest of create runs on the staged copy.
+struct StagedInstance {
+    spfom_instance in{};
+    std::vector<int64_t> seg_ptr, bundle_ptr;
+    std::vector<int32_t> prod_idx, bundle_res;
+    std::vector<double> attract, shadow, no_purchase, arrival, price, capacity, resource_capacity;
+};
+template <typename T>
+bool stage_array(std::vector<T> &dst, const T *src, int64_t n) {
+    if (!src || n <= 0) return true;
+    dst.resize((size_t)n);
+    return cudaMemcpy(dst.data(), src, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost) == cudaSuccess;
+}
+// in points at caller device memory; on success out.in points at host copies
+spfom_status stage_instance(const spfom_instance *in, StagedInstance &out) {
+    out.in = *in;
+    out.in.on_device = 0;
+    const int64_t m = in->num_segments, N = in->num_products, T = std::max<int64_t>(1, in->num_periods);
+    if (m < 0 || N < 1 || in->nnz < 0 || !in->seg_ptr) return fail(nullptr, SPFOM_EINVAL, "instance: missing array or bad size");
+    bool ok = stage_array(out.seg_ptr, in->seg_ptr, m + 1) && stage_array(out.prod_idx, in->prod_idx, in->nnz) &&
+              stage_array(out.attract, in->attract, in->nnz) && stage_array(out.shadow, in->shadow, in->nnz) &&
+              stage_array(out.no_purchase, in->no_purchase, m) && stage_array(out.arrival, in->arrival, T * m) &&
+              stage_array(out.price, in->price, N) && stage_array(out.capacity, in->capacity, N);
+    if (ok && in->num_resources > 0 && in->bundle_ptr) {
+        ok = stage_array(out.bundle_ptr, in->bundle_ptr, N + 1) &&
+             stage_array(out.resource_capacity, in->resource_capacity, in->num_resources);
+        if (ok && !out.bundle_ptr.empty()) ok = stage_array(out.bundle_res, in->bundle_res, out.bundle_ptr[N]);
+    }
+    if (!ok) return fail(nullptr, SPFOM_EINVAL, "instance: on_device arrays are not readable device memory");
+    auto P = [](auto &v, auto *orig) { return orig ? v.data() : nullptr; };
+    out.in.seg_ptr = P(out.seg_ptr, in->seg_ptr);
+    out.in.prod_idx = P(out.prod_idx, in->prod_idx);
+    out.in.attract = P(out.attract, in->attract);
+    out.in.shadow = P(out.shadow, in->shadow);
+    out.in.no_purchase = P(out.no_purchase, in->no_purchase);
+    out.in.arrival = P(out.arrival, in->arrival);
+    out.in.price = P(out.price, in->price);
+    out.in.capacity = P(out.capacity, in->capacity);
+    out.in.bundle_ptr = P(out.bundle_ptr, in->bundle_ptr);
+    out.in.bundle_res = P(out.bundle_res, in->bundle_res);
+    out.in.resource_capacity = P(out.resource_capacity, in->resource_capacity);
+    return SPFOM_OK;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ API
@@ -560,6 +642,12 @@ spfom_status spfom_nccl_unique_id(void *out128) {
 spfom_status spfom_workspace_bytes(const spfom_instance *inst, const spfom_params *params, size_t *bytes) {
     if (!inst || !bytes || !inst->seg_ptr || inst->num_segments < 0 || inst->num_products < 1)
         return fail(nullptr, SPFOM_EINVAL, "spfom_workspace_bytes: bad arguments");
+    StagedInstance staged;
+    if (inst->on_device) {
+        spfom_status st = stage_instance(inst, staged);
+        if (st != SPFOM_OK) return st;
+        inst = &staged.in;
+    }
     Plan pl;
     make_plan(inst, params, pl);
     *bytes = pl.total;
@@ -688,6 +776,13 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     if (!in || !out) return fail(nullptr, SPFOM_EINVAL, "spfom_create: NULL argument");
     *out = nullptr;
     PhaseTimer ptimer;
+    StagedInstance staged;
+    if (in->on_device) {
+        spfom_status sst = stage_instance(in, staged);
+        if (sst != SPFOM_OK) return sst;
+        in = &staged.in;
+        ptimer.mark("stage device instance");
+    }
     spfom_status st = validate(in, p);
     ptimer.mark("validate");
     if (st != SPFOM_OK) return st;
@@ -718,6 +813,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     h->T = pl.T;
     int dev = 0;
     cudaGetDevice(&dev);
+    h->device = dev;
     cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev);
     auto bail = [&](spfom_status s) {
         g_create_error = h->err;
@@ -1160,6 +1256,7 @@ extern "C" {
 
 spfom_status spfom_step(spfom_handle *h, int64_t k) {
     if (!h || k < 0) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     if (h->small) return step_small(h, k);
     for (int64_t it = 0; it < k; ++it) {
         const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
@@ -1198,12 +1295,14 @@ static spfom_status fetch_duals(spfom_handle *h, const double *src, double *eta)
 
 spfom_status spfom_duals(spfom_handle *h, double *eta) {
     if (!h || !eta) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     spfom_status st = fetch_duals(h, h->S.eta, eta);
     return st != SPFOM_OK ? st : check_counters(h);
 }
 
 spfom_status spfom_usage(spfom_handle *h, double *s) {
     if (!h || !s) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     std::vector<double> tmp(h->N);
     CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.s_prev, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1276,12 +1375,14 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
 
 spfom_status spfom_primal(spfom_handle *h, double *y, double *y0) {
     if (!h) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     spfom_status st = fetch_primal(h, h->S.y, reinterpret_cast<const double *>(h->S.segv), 32, y, y0);
     return st != SPFOM_OK ? st : check_counters(h);
 }
 
 spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double *etabar) {
     if (!h) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     if (!h->pl.averaging) return fail(h, SPFOM_EINVAL, "averaging is off");
     spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, 8, ybar, y0bar);
     if (st != SPFOM_OK) return st;
@@ -1291,6 +1392,7 @@ spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double
 
 spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     if (!h || !out) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     DevState S = h->S;
     double *sf = slot_ptr<double>(h, O_TMP);
     CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));
@@ -1377,6 +1479,7 @@ spfom_status spfom_objective(spfom_handle *h, double *obj) {
 
 spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0, const double *eta, const double *s_prev) {
     if (!h) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     const int64_t T = h->T;
     if (y) {
         std::vector<double> tmp(4 * std::max<int64_t>(T * h->nq, 1), 0.0);
@@ -1417,6 +1520,17 @@ spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0,
         std::vector<double> t3(h->N + 1, 0.0);
         for (int64_t jn = 0; jn < h->N; ++jn) t3[jn] = s_prev[h->new2old[jn]];
         CUDA_TRY(h, cudaMemcpyAsync(h->S.s_prev, t3.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    } else if (y) {
+        // s_prev is A y of the current iterate (sampled mode: the running
+        // stale-inclusive usage, K3 adds this iteration's delta to it): a
+        // restored y without its usage gets a fresh A y (+ the cross-rank sum)
+        double *sf = slot_ptr<double>(h, O_TMP);
+        CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));
+        k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(h->S, T * h->nq, sf, (int32_t)std::min<int64_t>(kHeadMax, h->N));
+        CUDA_TRY(h, cudaGetLastError());
+        spfom_status st = allreduce(h, sf, sf, (size_t)h->N, kNcclFloat64, kNcclSum);
+        if (st != SPFOM_OK) return st;
+        CUDA_TRY(h, cudaMemcpyAsync(h->S.s_prev, sf, h->N * 8, cudaMemcpyDeviceToDevice, h->stream));
     }
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     return SPFOM_OK;
@@ -1452,6 +1566,7 @@ spfom_status spfom_info(const spfom_handle *h_, spfom_info_t *out) {
 
 spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms) {
     if (!h || !ms || iters < 1) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     cudaEvent_t ev[3];
     for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
     double acc0 = 0.0, acc1 = 0.0;
@@ -1480,6 +1595,7 @@ spfom_status spfom_time_kernels(spfom_handle *h, int64_t iters, double *ms) {
 
 spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
     if (!h || !ms || k < 1) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     if (h->small) {
         // the persistent small-regime kernel runs whole iterations: one event pair
         // around all of them; the primal share is not separable (ms[0] = ms[1])
@@ -1540,10 +1656,11 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
 template <int KM>
 void launch_recover_km(spfom_handle *h, int64_t a, int64_t b, int64_t t) {
     constexpr int W = recover_warps<KM>();
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice cache;
+    int &attr = *cache.slot();
+    if (attr < 0) {
         cudaFuncSetAttribute(k_recover<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RecoverSmem<KM>));
-        attr = true;
+        attr = 1;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_recover<KM>, 32 * W, sizeof(RecoverSmem<KM>));
@@ -1577,6 +1694,7 @@ extern "C" {
 
 spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
     if (!h || !order || !alpha) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     const int64_t CH = recover_chunk(h->nq), m = h->m;
     std::vector<int32_t> qoff(m + 1);
     CUDA_TRY(h, cudaMemcpyAsync(qoff.data(), h->S.qoff, (m + 1) * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1611,6 +1729,7 @@ spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha) {
 
 spfom_status spfom_recover_timed(spfom_handle *h, double *ms) {
     if (!h || !ms) return SPFOM_EINVAL;
+    DeviceGuard dg_(h->device);
     const int64_t CH = recover_chunk(h->nq), m = h->m;
     std::vector<int32_t> qoff(m + 1);
     CUDA_TRY(h, cudaMemcpyAsync(qoff.data(), h->S.qoff, (m + 1) * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1640,6 +1759,7 @@ const char *spfom_last_error(const spfom_handle *h) { return h ? h->err.c_str() 
 
 void spfom_destroy(spfom_handle *h) {
     if (!h) return;
+    DeviceGuard dg_(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->graph_refresh) cudaGraphExecDestroy(h->graph_refresh);

@@ -21,20 +21,17 @@ namespace spfom {
 // stale rows kept); st = s_new + omega_x (s_new - s_prev);
 // eta = max(0, (1 - tau mu) eta - tau (c - st)); g = r - eta; s_prev = s_new;
 // acc = 0.  a8 (averaging): etabar += (eta - etabar) / t.
-// tick != 0 (no averaging): the last block to finish also advances the
-// iteration counter (one launch less per iteration than a separate k_tick).
+// tick != 0 (no averaging): the kernel also advances the iteration counter
+// (one launch less per iteration than a separate k_tick).
 __global__ void k_tick(int64_t *t) { *t += 1; }
 
-// last block of a grid advances the iteration counter (fused tick)
-__device__ __forceinline__ void tick_last_block(const DevState &S) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(S.counters + 3, 1ull) == (unsigned long long)gridDim.x - 1ull) {
-            *S.t += 1;
-            S.counters[3] = 0;
-        }
-    }
+// Fused tick: the kernels that tick never read *S.t themselves (only the
+// averaging path reads it, and that path ticks in a separate k_tick), and the
+// next reader is a later kernel on the same stream, so one thread of block 0
+// can advance the counter without waiting for the other blocks (no fence, no
+// arrival counter).
+__device__ __forceinline__ void tick_once(const DevState &S) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *S.t += 1;
 }
 
 // a7 for one product j (Eq. 17 with extrapolation and per-product tau_j)
@@ -72,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int
     const int64_t t_next = tick ? 0 : *S.t + 1;     // t is only needed for averaging (tick == 0)
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.N; j += (int64_t)gridDim.x * blockDim.x)
         dual_update(S, j, full, t_next);
-    if (tick) tick_last_block(S);
+    if (tick) tick_once(S);
 }
 
 // ----------------------------------------------------------------- bundles (a7, NRM)
@@ -108,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_bundle_prices(DevState S, int32_t 
         for (int32_t e = S.bptr[j]; e < S.bptr[j + 1]; ++e) b += S.eta[S.bres[e]];
         S.g[j] = S.r[j] - b;
     }
-    if (tick) tick_last_block(S);
+    if (tick) tick_once(S);
 }
 
 // Residual terms of the resource rows (bundles): partials[8] per block as in

@@ -42,7 +42,7 @@ class _Instance(C.Structure):
                 ("shadow", C.c_void_p), ("no_purchase", C.c_void_p), ("arrival", C.c_void_p),
                 ("price", C.c_void_p), ("capacity", C.c_void_p), ("num_periods", C.c_int64),
                 ("num_resources", C.c_int64), ("bundle_ptr", C.c_void_p), ("bundle_res", C.c_void_p),
-                ("resource_capacity", C.c_void_p)]
+                ("resource_capacity", C.c_void_p), ("on_device", C.c_int64)]
 
 
 class _Params(C.Structure):
@@ -85,13 +85,17 @@ def _base_of_stacked(inst, T: int) -> dict:
     seg_ptr = np.asarray(inst.seg_ptr[: m + 1], dtype=np.int64)
     tiled = dict(prod_idx=nb, attract=nb, shadow=nb, no_purchase=m)
     for name, n in tiled.items():
+        if getattr(inst, name, None) is None:
+            continue
         a = np.asarray(getattr(inst, name))
         if a.shape[0] != n * T or not np.array_equal(a.reshape(T, n), np.broadcast_to(a[:n], (T, n))):
             raise SpfomError(2, f"multi-period instance: {name} differs across periods (no shared structure)")
     if not np.array_equal(np.asarray(inst.seg_ptr).reshape(-1)[1:].reshape(T, m) - np.arange(T)[:, None] * nb,
                           np.broadcast_to(seg_ptr[1:], (T, m))):
         raise SpfomError(2, "multi-period instance: consideration sets differ across periods")
-    return dict(seg_ptr=seg_ptr, prod_idx=inst.prod_idx[:nb], attract=inst.attract[:nb], shadow=inst.shadow[:nb],
+    shadow = getattr(inst, "shadow", None)
+    return dict(seg_ptr=seg_ptr, prod_idx=inst.prod_idx[:nb], attract=inst.attract[:nb],
+                shadow=None if shadow is None else shadow[:nb],
                 no_purchase=inst.no_purchase[:m], arrival=np.asarray(inst.arrival, dtype=np.float64))
 
 
@@ -190,6 +194,30 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def _is_cuda_tensor(a) -> bool:
+    return getattr(a, "is_cuda", False) is True
+
+
+def _host_array(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _dev_array(a, dtype):
+    import torch
+    tdt = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}[dtype]
+    return a.to(dtype=tdt).contiguous()
+
+
+def _len(a) -> int:
+    return int(a.shape[0])
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.data_ptr() if _is_cuda_tensor(a) else a.ctypes.data
+
+
 class Solver:
     """One spfom handle.  `inst` is any object with the CSR fields of
     spfom_instance (seg_ptr, prod_idx, attract, shadow, no_purchase, arrival,
@@ -208,43 +236,60 @@ class Solver:
         import torch  # device memory and streams only
 
         L = load_library()
-        if not torch.cuda.is_available():
-            raise SpfomError(4, "no CUDA device: the SPFOM path has no CPU fallback")
         self.params = params or Params()
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        arrays = dict(seg_ptr=inst.seg_ptr, prod_idx=inst.prod_idx, attract=inst.attract, shadow=inst.shadow,
-                      no_purchase=inst.no_purchase, arrival=inst.arrival)
+        arrays = dict(seg_ptr=inst.seg_ptr, prod_idx=inst.prod_idx, attract=inst.attract,
+                      shadow=getattr(inst, "shadow", None), no_purchase=inst.no_purchase, arrival=inst.arrival)
         # a period-major stacked multi-period instance goes to the shared-structure
         # layout (num_periods = T): base rows once, arrival [T][m]
         T = int((getattr(inst, "meta", None) or {}).get("T", 1) or 1)
         self.periods = T if (shared_periods and T > 1) else 1
+        # instance arrays already in device memory (torch CUDA tensors): passed as
+        # device pointers (spfom_instance.on_device = 1), staged by the library
+        on_dev = [_is_cuda_tensor(a) for a in list(arrays.values()) + [inst.price, inst.capacity] if a is not None]
+        on_device = bool(on_dev) and all(on_dev)
+        if any(on_dev) and not on_device:
+            raise SpfomError(1, "instance arrays must be all host arrays or all CUDA tensors")
+        if on_device and self.periods > 1:
+            raise SpfomError(1, "device-resident instances: pass the base rows with num_periods (host layout check)")
         if self.periods > 1:
             arrays = _base_of_stacked(inst, T)
-        self._keep = dict(
-            seg_ptr=np.ascontiguousarray(arrays["seg_ptr"], dtype=np.int64),
-            prod_idx=np.ascontiguousarray(arrays["prod_idx"], dtype=np.int32),
-            attract=_f64(arrays["attract"]), shadow=_f64(arrays["shadow"]), no_purchase=_f64(arrays["no_purchase"]),
-            arrival=_f64(arrays["arrival"]), price=_f64(inst.price), capacity=_f64(inst.capacity))
-        k = self._keep
-        mb = k["seg_ptr"].shape[0] - 1
-        nb = k["prod_idx"].shape[0]
+        conv = _dev_array if on_device else _host_array
+        k = self._keep = dict(
+            seg_ptr=conv(arrays["seg_ptr"], np.int64), prod_idx=conv(arrays["prod_idx"], np.int32),
+            attract=conv(arrays["attract"], np.float64),
+            shadow=None if arrays["shadow"] is None else conv(arrays["shadow"], np.float64),
+            no_purchase=conv(arrays["no_purchase"], np.float64), arrival=conv(arrays["arrival"], np.float64),
+            price=conv(inst.price, np.float64), capacity=conv(inst.capacity, np.float64))
+        mb = _len(k["seg_ptr"]) - 1
+        nb = _len(k["prod_idx"])
         self.m = mb * self.periods            # stacked sizes: the getters' shapes
-        self.N = k["price"].shape[0]
+        self.N = _len(k["price"])
         self.nnz = nb * self.periods
+        # every length the library reads is checked here (it trusts the sizes)
+        want = dict(attract=nb, shadow=nb, no_purchase=mb, arrival=self.periods * mb, capacity=self.N)
+        for name, n in want.items():
+            if k[name] is not None and _len(k[name]) != n:
+                raise SpfomError(1, f"instance: len({name}) = {_len(k[name])}, expected {n}")
+        if mb < 0 or self.N < 1:
+            raise SpfomError(1, "instance: need seg_ptr of length m + 1 >= 1 and at least one product")
         # bundles / NRM: duals per resource
         self.L = int(getattr(inst, "num_resources", 0) or 0)
         if self.L > 0:
-            k.update(bundle_ptr=np.ascontiguousarray(inst.bundle_ptr, dtype=np.int64),
-                     bundle_res=np.ascontiguousarray(inst.bundle_res, dtype=np.int32),
-                     resource_capacity=_f64(inst.resource_capacity))
+            k.update(bundle_ptr=conv(inst.bundle_ptr, np.int64), bundle_res=conv(inst.bundle_res, np.int32),
+                     resource_capacity=conv(inst.resource_capacity, np.float64))
+            if _len(k["bundle_ptr"]) != self.N + 1 or _len(k["resource_capacity"]) != self.L:
+                raise SpfomError(1, "instance: bundle_ptr needs N + 1 entries and resource_capacity L")
         self.n_duals = self.L if self.L > 0 else self.N
+        if not torch.cuda.is_available():
+            raise SpfomError(4, "no CUDA device: the SPFOM path has no CPU fallback")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._inst = _Instance(mb, self.N, nb, int(segment_offset),
                                int(num_segments_global if num_segments_global is not None else mb),
-                               *[k[n].ctypes.data for n in ("seg_ptr", "prod_idx", "attract", "shadow",
-                                                            "no_purchase", "arrival", "price", "capacity")],
+                               *[_ptr(k[n]) for n in ("seg_ptr", "prod_idx", "attract", "shadow",
+                                                      "no_purchase", "arrival", "price", "capacity")],
                                self.periods, self.L,
-                               *([k[n].ctypes.data for n in ("bundle_ptr", "bundle_res", "resource_capacity")]
-                                 if self.L > 0 else [None] * 3))
+                               *([_ptr(k[n]) for n in ("bundle_ptr", "bundle_res", "resource_capacity")]
+                                 if self.L > 0 else [None] * 3), int(on_device))
         self._params, self._blocks = self.params._c()
         nbytes = C.c_size_t()
         _check(L.spfom_workspace_bytes(C.byref(self._inst), C.byref(self._params), C.byref(nbytes)))

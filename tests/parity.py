@@ -20,27 +20,31 @@ def oracle_kwargs(p) -> dict:
                 averaging=p.averaging, refresh_every=p.refresh_every)
 
 
-def lockstep(inst, params, iters: int, blocks=None, check_every: int = 1, tie_margin=None):
+def lockstep(inst, params, iters: int, blocks=None, check_every: int = 1, tie_margin=None, check_first: int = 0,
+             gpu=None):
     """Run GPU and oracle side by side; return the worst per-iteration errors
-    (y, y0, eta) over iterations 1..iters."""
+    (y, y0, eta) over iterations 1..iters.  Checked after every iteration t with
+    t <= check_first, t % check_every == 0, and the last one.  `gpu`: an
+    already created Solver for `inst` (at iteration 0)."""
     import oracle
     from paper_2602_22421_b200 import Solver
 
-    gpu = Solver(inst, params)
+    gpu = gpu if gpu is not None else Solver(inst, params)
     cpu = oracle.OracleSolver(inst, **oracle_kwargs(params))
     ys, lams, rs = 1.0, float(inst.arrival.max()), float(inst.price.max())
     worst = dict(y=0.0, y0=0.0, eta=0.0, s=0.0)
     for t in range(iters):
         gpu.step(1)
         cpu.step(None if blocks is None else blocks[t % blocks.shape[0]])
-        if (t + 1) % check_every == 0 or t + 1 == iters:
+        if (t + 1) % check_every == 0 or t + 1 == iters or t + 1 <= check_first:
             y, y0 = gpu.primal()
             eta = gpu.duals()
             s = gpu.usage()
             e = dict(y=rel_inf(y, cpu.y, lams), y0=rel_inf(y0, cpu.y0, lams), eta=rel_inf(eta, cpu.eta, rs),
                      s=rel_inf(s, cpu.s, lams))
-            for k in worst:
+            for k in e:
                 worst[k] = max(worst[k], e[k])
+            worst["checks"] = worst.get("checks", 0) + 1
             if max(e.values()) > TOL_ITER:
                 worst["first_bad_iter"] = t + 1
                 break

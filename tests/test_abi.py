@@ -156,3 +156,18 @@ def test_ctypes_mirrors_match_the_header_structs(lib):
     lib.spfom_abi_sizes(out)
     assert list(out) == [C.sizeof(B._Instance), C.sizeof(B._Params), C.sizeof(B._Info), C.sizeof(B._Residuals),
                          C.sizeof(B._Dist)]
+
+
+def test_binding_checks_array_lengths_before_native_code():
+    """The C ABI trusts the sizes it is given: the binding rejects short arrays
+    (SPFOM_EINVAL) before any pointer reaches the library (no GPU needed)."""
+    import copy
+    from paper_2602_22421_b200 import Solver, SpfomError
+    from spfom_inputs import generate
+    inst = generate("tiny")
+    for field, cut in (("attract", 1), ("shadow", 1), ("no_purchase", 1), ("arrival", 1), ("capacity", 1)):
+        bad = copy.copy(inst)
+        setattr(bad, field, np.asarray(getattr(inst, field))[:-cut])
+        with pytest.raises(SpfomError) as ei:
+            Solver(bad)
+        assert ei.value.status == 1, (field, ei.value)

@@ -208,6 +208,88 @@ def test_checkpoint_resume():
     b.close()
 
 
+@pytest.mark.parametrize("sampled", [False, True])
+def test_set_state_without_usage_recomputes_it(sampled):
+    """spfom_set_state(y, y0, eta) without s_prev: the library recomputes
+    s_prev = A y, so the resumed run equals the uninterrupted one (sampled
+    mode: s_prev is the running stale-inclusive usage the next dual step adds
+    its delta to)."""
+    from paper_2602_22421_b200 import Solver
+    inst = generate("small", m=400, N=200, k=(5, 60))
+    blocks = block_sequence(inst.m, 90, 40, seed=4) if sampled else None
+    p = _params(blocks=blocks, exec_mode=1)
+    a = Solver(inst, p)
+    a.step(20)
+    y, y0 = a.primal()
+    eta = a.duals()
+    b = Solver(inst, p)
+    b.step(20)                      # same block cursor; state then overwritten
+    b.set_state(y=np.zeros_like(y), y0=inst.arrival.copy(), eta=np.zeros_like(eta))
+    b.set_state(y=y, y0=y0, eta=eta)
+    assert rel_inf(b.usage(), a.usage(), 1.0) <= 1e-12
+    a.step(10)
+    b.step(10)
+    ya, _ = a.primal()
+    yb, _ = b.primal()
+    assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
+def test_shadow_none_is_mnl():
+    """shadow = NULL in the C ABI means MNL (w = 0): identical to explicit zeros."""
+    import copy
+    from paper_2602_22421_b200 import Solver
+    inst = generate("small", m=300, N=150, k=(5, 40))
+    inst.shadow[:] = 0.0
+    inst2 = copy.copy(inst)
+    inst2.shadow = None
+    a, b = Solver(inst, _params()), Solver(inst2, _params())
+    a.step(15)
+    b.step(15)
+    # equal up to the order of K1's fp64 global reductions (not fixed run to run)
+    assert rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
+def test_device_resident_instance():
+    """spfom_instance.on_device = 1: torch CUDA tensors as the instance arrays
+    give the same iterates as host arrays."""
+    import copy
+    import torch
+    from paper_2602_22421_b200 import Solver
+    inst = generate("medium", m=2000, N=1200, k=(20, 200))
+    dev = copy.copy(inst)
+    for f in ("seg_ptr", "prod_idx", "attract", "shadow", "no_purchase", "arrival", "price", "capacity"):
+        setattr(dev, f, torch.from_numpy(np.ascontiguousarray(getattr(inst, f))).cuda())
+    a, b = Solver(inst, _params()), Solver(dev, _params())
+    a.step(10)
+    b.step(10)
+    ya, _ = a.primal()
+    yb, _ = b.primal()
+    assert rel_inf(yb, ya, 1.0) <= 1e-12 and rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2")
+def test_two_devices_in_one_process():
+    """Distinct handles on distinct GPUs are independent (per-device kernel
+    attributes; every entry point runs on its handle's device)."""
+    import torch
+    from paper_2602_22421_b200 import Solver
+    inst = generate("medium", m=3000, N=1500, k=(20, 200))
+    a = Solver(inst, _params(), device="cuda:0")
+    b = Solver(inst, _params(), device="cuda:1")
+    torch.cuda.set_device(0)
+    a.step(5)
+    b.step(5)
+    assert rel_inf(b.duals(), a.duals(), 1.0) <= 1e-12
+    a.close()
+    b.close()
+
+
 def test_step_timed_is_step():
     """The timed stepping bench.py uses (two graphs per iteration, events around
     the primal graph) computes the same iterates as spfom_step."""
