@@ -500,6 +500,12 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
         full_mode = 1;
         ++nl;
     }
+#ifdef SPFOM_DIAG_SEP_USAGE
+    // diagnostic: the usage of the iteration recomputed from y (K1's scatter off or discarded)
+    CUDA_TRY(h, cudaMemsetAsync(acc, 0, (h->N + 1) * 8, h->stream));
+    if (S.spread_n > 0) CUDA_TRY(h, cudaMemsetAsync(S.spread, 0, (size_t)S.spread_c * S.spread_n * 8, h->stream));
+    k_usage<<<h->sm_count * 4, kThreads, 0, h->stream>>>(S, h->T * h->nq, acc, (int32_t)std::min<int64_t>(kHeadMax, h->N));
+#endif
     if (h->comm && S.spread_n > 0) {
         // fold the spread copies into acc before the cross-rank sum
         k_fold<<<std::max<int64_t>(1, (S.spread_n + kThreads - 1) / kThreads), kThreads, 0, h->stream>>>(S);
@@ -1781,6 +1787,16 @@ void spfom_destroy(spfom_handle *h) {
 
 }  // extern "C"
 
+#ifdef SPFOM_DIAG_PHASE
+extern "C" int spfom_diag_phase(unsigned long long *out, int reset) {
+    int e = (int)cudaMemcpyFromSymbol(out, spfom::g_diag_phase, 10 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(spfom::g_diag_phase, z, sizeof z);
+    }
+    return e;
+}
+#endif
 #ifdef SPFOM_DIAG_TIME
 extern "C" int spfom_diag_time(uint64_t *out, int n) {
     return (int)cudaMemcpyFromSymbol(out, spfom::g_diag_time, sizeof(uint64_t) * (size_t)n);

@@ -49,6 +49,26 @@
 
 namespace spfom {
 
+#ifndef SPFOM_FAST_RCP
+#define SPFOM_FAST_RCP 1
+#endif
+// 1 / x to full double precision (within an ulp, not correctly rounded): the
+// MUFU seed refined by two Newton steps -- ~50 cycles of dependent latency
+// instead of ~130 for the IEEE division (B200, exp/ubench_fp64.cu).  Used for
+// the Newton direction only, a search step, not an output.
+__device__ __forceinline__ double fast_rcp(double x) {
+#if SPFOM_FAST_RCP
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+#else
+    return 1.0 / x;
+#endif
+}
+
 // Solve J d = -R (3x3) by cofactors; false if singular / non-finite.
 __device__ __forceinline__ bool newton_dir(const double J[3][3], const double R[3], double d[3]) {
     const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
@@ -56,7 +76,7 @@ __device__ __forceinline__ bool newton_dir(const double J[3][3], const double R[
     const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
     const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
     if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
-    const double inv = 1.0 / det;
+    const double inv = fast_rcp(det);
     const double c10 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
     const double c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
     const double c12 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
@@ -137,6 +157,46 @@ __device__ __forceinline__ double y_entry(double z, double v, double om, double 
     return y;
 }
 
+#ifndef SPFOM_CHECK_OUT
+#define SPFOM_CHECK_OUT 1
+#endif
+// CHECK pass + output, one entry: class bits at (x0, x1, x2) and
+// y_j = clamp(a_j, 0, v_j U) from the same two comparisons (entry-mapped
+// stream kernels; in the 168-register 12-warp layouts the extra live y values
+// spill, so they keep the separate output pass).
+__device__ __forceinline__ double check_out(double z, double v, double om, double x0, double x1, double x2,
+                                            uint32_t bit, uint32_t &cm, uint32_t &fm) {
+    const double a = fma(om, x1, z - x0);
+    const double cap = v * x2;
+    double y;
+    asm("{\n\t.reg .pred pc, pf;\n\t.reg .f64 t;\n\t"
+        "setp.ge.f64 pc, %3, %4;\n\t"
+        "setp.gt.and.f64 pf, %3, 0d0000000000000000, !pc;\n\t"
+        "@pc or.b32 %0, %0, %5;\n\t"
+        "@pf or.b32 %1, %1, %5;\n\t"
+        "selp.f64 t, %3, 0d0000000000000000, pf;\n\t"
+        "selp.f64 %2, %4, t, pc;\n\t}"
+        : "+r"(cm), "+r"(fm), "=d"(y)
+        : "d"(a), "d"(cap), "r"(bit));
+    return y;
+}
+
+// Diagnostics (exp/phase.py, exp/k1var.py; never in the product build):
+//   SPFOM_DIAG_PHASE        cycles per phase of a K1 stream round (g_diag_phase)
+//   SPFOM_DIAG_SKIP_PROJECT no projection (y <- a function of z): data movement only
+//   SPFOM_DIAG_SKIP_RED     no global reductions in the stream kernel
+//   SPFOM_DIAG_RED_FROM=j0  global reductions only for products >= j0
+//   SPFOM_DIAG_SEP_USAGE    no usage scatter in K1; A y recomputed by k_usage before K3
+//                           (+ SPFOM_DIAG_SEP_DUMMY: K1 still scatters, into discarded copies)
+#ifdef SPFOM_DIAG_PHASE
+// [0] mbarrier wait, [1] slot read + gather + step, [2] projection, [3] y /
+// state write-back, [4] head histograms, [5] global reductions, [6] rounds,
+// [7] loop / claim, [8] TMA issue
+__device__ unsigned long long g_diag_phase[10];
+#define PH_MARK(k) do { const long long t_ = clock64(); ph[k] += t_ - ph_t; ph_t = t_; } while (0)
+#else
+#define PH_MARK(k) do { } while (0)
+#endif
 #ifdef SPFOM_DIAG_TIME
 __device__ uint64_t g_diag_time[2 * 148 * 16];   // diagnostic: per-warp start / end of the last K1 launch
 __device__ uint32_t g_diag_loops[4 * 148 * 16];  // diagnostic: per warp: mbarrier-wait, scatter kcycles, smid
@@ -149,7 +209,7 @@ struct ProjStats {
 // this G-lane group (reading c5).  (x0, x1, x2) holds the warm
 // start (nu, kappa, U) on entry and the final multipliers on exit; yv / y0new
 // receive the projected point.  Must be called by the whole warp.
-template <int G, int NE>
+template <int G, int NE, bool CO = false>
 __device__ __forceinline__ void project_group(const double (&z)[NE], const double (&v)[NE], const double (&om)[NE],
                                               double z0, double lam, double vt0, bool active, unsigned gmask,
                                               int max_newton, double &x0, double &x1, double &x2,
@@ -164,6 +224,7 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
     double d0 = 0.0, d1 = 0.0, d2 = 0.0, step = 1.0, Ra = 0.0;
     uint32_t cA = 0, fA = 0;                            // class bitmasks at the accepted point
     bool go = active, full = true, first = true, failed = false, restarted = false;
+    bool have_y = false;                                // yv formed by the final CHECK pass
     int passes = 0;
     const int restart_at = max_newton / 2;
     while (__any_sync(0xffffffffu, go)) {
@@ -200,13 +261,27 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
         uint32_t cm = 0, fm = 0;
         if (!need) {
             // CHECK pass for every unfinished group of the warp
+            if constexpr (CO && SPFOM_CHECK_OUT) {
+                // ... which also forms y at the point (the same a and cap): when it
+                // ends the loop for every group of the warp, that is the output
+                // (groups finished earlier re-evaluate at their final multipliers)
 #pragma unroll
-            for (int e = 0; e < NE; ++e) check_bits(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
+                for (int e = 0; e < NE; ++e) yv[e] = check_out(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
+            } else {
+#pragma unroll
+                for (int e = 0; e < NE; ++e) check_bits(z[e], v[e], om[e], x0, x1, x2, 1u << e, cm, fm);
+            }
             const bool changed = (__ballot_sync(0xffffffffu, (cm != cA) || (fm != fA)) & gmask) != 0u;
             if (go) {
                 ++passes;
                 if (!changed) go = false;     // same piece: R(x) = 0 exactly
                 else full = true;             // piece moved: evaluate R, J here
+            }
+            if constexpr (CO && SPFOM_CHECK_OUT) {
+                if (!__any_sync(0xffffffffu, go)) {
+                    have_y = true;
+                    break;
+                }
             }
             continue;
         }
@@ -284,8 +359,10 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
         st.restarts += restarted ? 1ull : 0ull;
 #endif
     }
+    if (!have_y) {
 #pragma unroll
-    for (int e = 0; e < NE; ++e) yv[e] = y_entry(z[e], v[e], om[e], x0, x1, x2);
+        for (int e = 0; e < NE; ++e) yv[e] = y_entry(z[e], v[e], om[e], x0, x1, x2);
+    }
     y0new = z0 - x0 + x1;
 }
 
@@ -569,8 +646,13 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
     uint32_t phase = 0;
+#ifdef SPFOM_DIAG_PHASE
+    long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph_t = clock64();
+#endif
     for (; q0 >= 0; q0 = q1, q1 = q2, q2 = fnext(), phase ^= 1u) {
         const int64_t r = q0;
+        PH_MARK(7);
 #ifdef SPFOM_DIAG_TIME
         const long long tw0 = clock64();
         mbar_wait(bar, phase);
@@ -579,6 +661,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 #else
         mbar_wait(bar, phase);
 #endif
+        PH_MARK(0);
         // round q1's offsets from the window that arrived with this round
         int32_t qn = 0;
         if (q1 >= 0) {
@@ -661,8 +744,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         // issued (the consumer-release pattern of TMA pipelines); a
         // fence.proxy.async here compiles to MEMBAR.ALL.CTA, which would also
         // wait for the previous round's global reductions to drain.
+        PH_MARK(1);
         __syncwarp();
         if (q1 >= 0) issue(q1, qn, q2);
+        PH_MARK(8);
 
         // a2: price gather (g[N] = 0 for pads; head from shared memory).  The
         // opaque copies keep the two bases in registers (otherwise ptxas
@@ -683,8 +768,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         double yv[NE];
         double y0new;
         double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+        PH_MARK(1);
+#ifdef SPFOM_DIAG_SKIP_PROJECT
+#pragma unroll
+        for (int e = 0; e < NE; ++e) yv[e] = z[e] * v[e] + om[e];
+        y0new = z0;
+        (void)lam; (void)vt0;
+#else
         if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
-        else project_group<G, NE>(z, v, om, z0, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
+        else project_group<G, NE, (EQ > 0)>(z, v, om, z0, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
+#endif
+        PH_MARK(2);
 
         // ---- write back (y, segment state), a5 usage scatter
         if constexpr (EQ > 0) {
@@ -705,12 +799,14 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             if (q < qb) st256_stream(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+        PH_MARK(3);
 #ifdef SPFOM_DIAG_TIME
         const long long ts0 = clock64();
 #endif
         // a5: head -> histogram, warm head -> spread copies, tail -> s
         // ids are distinct within a segment and every group has its own
         // histogram: all loads first, then all stores (no serial RMW chain)
+#if !defined(SPFOM_DIAG_SEP_USAGE) || defined(SPFOM_DIAG_SEP_DUMMY)
         {
             double hv[NE];
 #pragma unroll
@@ -719,18 +815,33 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             for (int e = 0; e < NE; ++e)
                 if (idx[e] < HH) sts_f64(hg_s + 8u * (uint32_t)idx[e], hv[e] + yv[e]);
         }
+#endif
+        PH_MARK(4);
+#if !defined(SPFOM_DIAG_SKIP_RED) && (!defined(SPFOM_DIAG_SEP_USAGE) || defined(SPFOM_DIAG_SEP_DUMMY))
+#ifndef SPFOM_DIAG_RED_FROM
+#define SPFOM_DIAG_RED_FROM HH
+#endif
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
             const int off = j < spread_n ? spread_rel + j : j;     // warm head -> this warp's spread copy
-            red_add_if(S.s + off, yv[e], j >= HH && j < N);
+            red_add_if(S.s + off, yv[e], j >= SPFOM_DIAG_RED_FROM && j < N);
         }
+#endif
 #ifdef SPFOM_DIAG_TIME
         red_cycles += clock64() - ts0;
         (void)tr0;
 #endif
         qc = qn;
+        PH_MARK(5);
+#ifdef SPFOM_DIAG_PHASE
+        ph[6] += 1;
+#endif
     }
+#ifdef SPFOM_DIAG_PHASE
+    if (lane == 0)
+        for (int k = 0; k < 10; ++k) atomicAdd(&g_diag_phase[k], (unsigned long long)ph[k]);
+#endif
 #ifdef SPFOM_DIAG_TIME
     if (lane == 0) {
         g_diag_loops[4 * (blockIdx.x * LY::WARPS + warp)] = (uint32_t)(wait_cycles >> 10);
