@@ -17,6 +17,7 @@ for target in [5, 1500]:
     rounds = float(buf[6])
     print(f"iter {target}: K1 {k1/20:.4f} ms, rounds {rounds/20:.0f}/launch; cycles per warp-round:")
     tot = sum(float(buf[k]) for k in range(10) if k != 6)
+    print(f"   scatter warps busy per handed-over round: {float(buf[9]) / max(rounds, 1):8.0f}")
     for k in range(10):
         if k not in (6, 9):
             print(f"   {names[k]:18s} {float(buf[k]) / rounds:8.0f}  ({100 * float(buf[k]) / tot:4.1f}%)")
