@@ -417,15 +417,19 @@ def main():
     barrier()
     torch.cuda.synchronize(device)
     ev0.record(stream)
-    # each iteration = primal graph + rest graph, CUDA events around the primal
-    # kernels on the solver's stream (roofline.achieved is live, over this region)
+    # each iteration = one replay of the iteration graph (4 iterations per graph
+    # launch), whose event-record nodes bracket the primal kernels on the
+    # solver's stream (roofline.achieved is live, over this region).  The
+    # region is the device time from the first iteration's first event to the
+    # event recorded after the last iteration (region_ms); ev0 / ev1 around
+    # the call also contain the host's event bookkeeping inside step_timed.
     primal_ms_sum, region_ms = solver.step_timed(args.steps)
     ev1.record(stream)
     torch.cuda.synchronize(device)
     barrier()
-    ms_local = ev0.elapsed_time(ev1)
+    ms_outer = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
-    ms = max_over_ranks(ms_local)
+    ms = max_over_ranks(region_ms)
     value = args.steps / (ms / 1e3)
     k1_ms = max_over_ranks(primal_ms_sum) / args.steps
     rest_ms = max(0.0, ms / args.steps - k1_ms)
@@ -484,11 +488,16 @@ def main():
                                         f"20 B/base nnz x {shard.nnz // T} + 16 B/nnz x {shard.nnz} + "
                                         f"4 B/base segment x {shard.m // T} + 32 B/segment x {shard.m} (T = {T} shared)"),
                          "k1_ms_avg": k1_ms, "rest_ms_avg": rest_ms, "k1_share_of_step": k1_ms / (ms / args.steps),
-                         "k1_timing": ("CUDA events on the solver stream around the primal graph of every timed iteration"
+                         "k1_timing": ("CUDA event-record nodes around the primal kernels of every timed iteration "
+                                       "(solver stream, inside the iteration graph)"
                                        if not info.get("persistent") else
                                        "persistent small-regime kernel (whole iterations): CUDA events around all of them"),
                          "peak_source": peak_src, "frac_of_8tbs": k1_achieved / 8000.0},
             "clocks": clocks,
+            "timed_region": {"device_ms": ms, "outer_events_ms": ms_outer,
+                             "note": "value = steps / device_ms: events on the solver stream from the first "
+                                     "iteration's start to the end of the last; outer_events_ms (events around "
+                                     "the step_timed call) also holds its host-side event bookkeeping"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                     "d2h_bytes_per_step": d2h / args.steps,
                     "definition": "wall time of Solver(host arrays) [validate+layout+H2D] + K graph-replayed "

@@ -290,13 +290,14 @@ spfom_status spfom_recover(spfom_handle *h, int32_t *order, double *alpha);
 spfom_status spfom_recover_timed(spfom_handle *h, double *ms);
 
 /* Timed stepping (bench.py's timed region): enqueue k iterations exactly like
- * spfom_step -- each iteration replays two CUDA graphs, the primal kernels
- * (a1-a5) and the rest (a6-a8 + tick), with a CUDA event recorded on the
- * handle's stream before and after the primal graph -- then synchronise and
- * write ms[0] = summed event time of the primal kernels over the k iterations,
- * ms[1] = event time from the first to the last event (all k iterations).
- * In the small regime (spfom_info.persistent) the iterations run inside the
- * persistent kernel: ms[0] = ms[1] = their event time.
+ * spfom_step -- one replay of the iteration's CUDA graph each, whose two
+ * event-record nodes (before and after the primal kernels a1-a5) are pointed at
+ * that iteration's pair of CUDA events before the launch (sampled refresh
+ * iterations use two graphs with the events between them) -- then synchronise
+ * and write ms[0] = summed event time of the primal kernels over the k
+ * iterations, ms[1] = event time from the first to the last event (all k
+ * iterations).  In the small regime (spfom_info.persistent) the iterations run
+ * inside the persistent kernel: ms[0] = ms[1] = their event time.
  * Collective when world > 1.  Advances the iterate by k. */
 spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms);
 

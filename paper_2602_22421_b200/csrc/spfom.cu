@@ -97,6 +97,10 @@ int bin_of(int64_t nq) {
 }
 
 constexpr int kResidBlocks = 592;   // 4 x 148 SMs
+#ifndef SPFOM_GRAPH_UNROLL
+#define SPFOM_GRAPH_UNROLL 4
+#endif
+constexpr int kGraphUnroll = SPFOM_GRAPH_UNROLL;   // iterations per CUDA graph in spfom_step (k >= this)
 
 // Per-device launch facts (opt-in shared memory set on the kernel, occupancy):
 // cudaFuncSetAttribute applies to the current device's context only, so a
@@ -205,7 +209,7 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_RESPROD] = (size_t)kResidBlocks * 8 * 8;
     sz[O_COUNTERS] = 8 * 8;
     sz[O_T] = 8;
-    sz[O_WORK] = 8 * kNumBins;   // K1 stream: dynamic round-chunk counters, one per bin
+    sz[O_WORK] = 16 * kNumBins;  // K1 stream: dynamic round-chunk counter + exited-block count, per bin
     sz[O_COUNTS] = N1 * 8;
     // recovery scratch (spfom_recover works in chunks of at most recover_chunk() padded entries)
     sz[O_RECORD] = (size_t)recover_chunk(pl.nq) * 4;
@@ -243,7 +247,15 @@ struct spfom_handle {
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
     int64_t iter = 0;
     cudaGraphExec_t graph = nullptr, graph_refresh = nullptr;
-    cudaGraphExec_t graph_primal = nullptr, graph_rest = nullptr, graph_rest_refresh = nullptr;   // split (timed) form
+    cudaGraphExec_t graph_u = nullptr;         // kGraphUnroll iterations in one graph (no refresh)
+    cudaGraphExec_t graph_primal = nullptr, graph_rest = nullptr, graph_rest_refresh = nullptr;   // split form (refresh iterations of spfom_step_timed)
+    // timed form: the iteration graph with an event-record node before and after
+    // the primal kernels; spfom_step_timed points them at fresh events per launch
+    // (timed_*[0]: one iteration, [1]: kGraphUnroll iterations)
+    cudaGraph_t graph_timed_src[2] = {nullptr, nullptr};
+    cudaGraphExec_t graph_timed[2] = {nullptr, nullptr};
+    std::vector<cudaGraphNode_t> timed_node[2];
+    std::vector<cudaEvent_t> timed_ev[2];
     std::string err;
     int sm_count = 148;
     int device = 0;                            // every entry point runs with this device current
@@ -452,13 +464,12 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 StreamList SL{};
                 SL.first = h->bin_first[b];
                 SL.count = cnt;
-                SL.work = slot_ptr<unsigned long long>(h, O_WORK) + b;
+                SL.work = slot_ptr<unsigned long long>(h, O_WORK) + 2 * b;   // reset by the launch's last block
                 SL.uni = h->bin_uniform[b] ? 1 : 0;
                 // several bins: concurrent persistent kernels on disjoint SM shares
                 // (forked streams; inside a graph they become parallel branches)
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
                 cudaStream_t st = h->nbins_active > 1 ? h->side[b] : h->stream;
-                CUDA_TRY(h, cudaMemsetAsync(SL.work, 0, 8, st));   // dynamic round chunks start at 0
                 if (h->T > 1) mp_dispatch(b, argmax, S, SL, sms, st);
                 else stream_dispatch(b, argmax, S, SL, sms, st);
                 ++nl;
@@ -539,11 +550,13 @@ spfom_status enqueue_iteration(spfom_handle *h, bool refresh) {
 }
 
 // part: 0 = whole iteration, 1 = primal kernels only, 2 = the rest
-spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, int part = 0) {
+spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, int part = 0, int iters = 1) {
     cudaGraph_t g;
     CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    spfom_status st = part == 0 ? enqueue_iteration(h, refresh)
-                    : part == 1 ? enqueue_primal(h, nullptr) : enqueue_rest(h, refresh, nullptr);
+    spfom_status st = SPFOM_OK;
+    for (int it = 0; it < iters && st == SPFOM_OK; ++it)
+        st = part == 0 ? enqueue_iteration(h, refresh)
+           : part == 1 ? enqueue_primal(h, nullptr) : enqueue_rest(h, refresh, nullptr);
     cudaGraph_t gg;
     cudaError_t e = cudaStreamEndCapture(h->stream, &gg);
     if (st != SPFOM_OK) return st;
@@ -552,6 +565,53 @@ spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, in
     e = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return SPFOM_OK;
+}
+
+// The timed iteration graph (u = 0: one iteration, 1: kGraphUnroll): per
+// iteration, event record -> primal kernels -> event record -> the rest (no
+// refresh).  cudaEventRecordExternal makes the records event-record nodes (a
+// plain record inside a capture only orders streams).
+spfom_status build_timed_graph(spfom_handle *h, int u) {
+    const int iters = u ? kGraphUnroll : 1;
+    h->timed_ev[u].assign(2 * iters, nullptr);
+    h->timed_node[u].assign(2 * iters, nullptr);
+    for (auto &e : h->timed_ev[u]) CUDA_TRY(h, cudaEventCreate(&e));
+    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    spfom_status st = SPFOM_OK;
+    for (int it = 0; it < iters && st == SPFOM_OK; ++it) {
+        if (cudaEventRecordWithFlags(h->timed_ev[u][2 * it], h->stream, cudaEventRecordExternal) != cudaSuccess)
+            st = fail(h, SPFOM_ECUDA, "timed graph: event record");
+        if (st == SPFOM_OK) st = enqueue_primal(h, nullptr);
+        if (st == SPFOM_OK &&
+            cudaEventRecordWithFlags(h->timed_ev[u][2 * it + 1], h->stream, cudaEventRecordExternal) != cudaSuccess)
+            st = fail(h, SPFOM_ECUDA, "timed graph: event record");
+        if (st == SPFOM_OK) st = enqueue_rest(h, false, nullptr);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (st != SPFOM_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("timed graph capture: ") + cudaGetErrorString(e));
+    h->graph_timed_src[u] = g;
+    size_t nn = 0;
+    CUDA_TRY(h, cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_TRY(h, cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (cudaGraphNode_t n : nodes) {
+        cudaGraphNodeType ty;
+        CUDA_TRY(h, cudaGraphNodeGetType(n, &ty));
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev = nullptr;
+        CUDA_TRY(h, cudaGraphEventRecordNodeGetEvent(n, &ev));
+        for (int k = 0; k < 2 * iters; ++k)
+            if (ev == h->timed_ev[u][k]) h->timed_node[u][k] = n;
+    }
+    for (cudaGraphNode_t n : h->timed_node[u])
+        if (!n) return fail(h, SPFOM_ECUDA, "timed graph: event nodes not found");
+    CUDA_TRY(h, cudaGraphInstantiate(&h->graph_timed[u], g, 0));
     return SPFOM_OK;
 }
 
@@ -828,6 +888,14 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             if (h->ev_join[b]) cudaEventDestroy(h->ev_join[b]);
         }
         if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+        for (cudaGraphExec_t g : {h->graph, h->graph_u, h->graph_refresh, h->graph_primal, h->graph_rest,
+                                  h->graph_rest_refresh, h->graph_timed[0], h->graph_timed[1]})
+            if (g) cudaGraphExecDestroy(g);
+        for (int u = 0; u < 2; ++u) {
+            if (h->graph_timed_src[u]) cudaGraphDestroy(h->graph_timed_src[u]);
+            for (cudaEvent_t e : h->timed_ev[u])
+                if (e) cudaEventDestroy(e);
+        }
         for (int c = 0; c < 2; ++c) {
             if (h->pin_ev[c]) cudaEventSynchronize(h->pin_ev[c]);
             if (h->pin[c]) cudaFreeHost(h->pin[c]);
@@ -1093,7 +1161,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
     ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, D1 * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
-         Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 8 * kNumBins);
+         Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 16 * kNumBins);
     if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, D1 * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
@@ -1202,11 +1270,13 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     }
     ptimer.mark("H2D + state + modes");
     st = build_graph(h, false, &h->graph);
-    if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
-    if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_rest, 2);
+    if (st == SPFOM_OK && !(pl.sampled && p->refresh_every > 0)) st = build_graph(h, false, &h->graph_u, 0, kGraphUnroll);
+    if (st == SPFOM_OK) st = build_timed_graph(h, 0);
+    if (st == SPFOM_OK && h->graph_u) st = build_timed_graph(h, 1);
     if (st != SPFOM_OK) return bail(st);
     if (pl.sampled && p->refresh_every > 0) {
         st = build_graph(h, true, &h->graph_refresh);
+        if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
         if (st == SPFOM_OK) st = build_graph(h, true, &h->graph_rest_refresh, 2);
         if (st != SPFOM_OK) return bail(st);
     }
@@ -1264,10 +1334,19 @@ spfom_status spfom_step(spfom_handle *h, int64_t k) {
     if (!h || k < 0) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
     if (h->small) return step_small(h, k);
-    for (int64_t it = 0; it < k; ++it) {
+    for (int64_t it = 0; it < k;) {
+        if (h->graph_u && k - it >= kGraphUnroll) {
+            // kGraphUnroll iterations per launch: their kernels follow each other
+            // inside one graph (no graph-to-graph gap)
+            CUDA_TRY(h, cudaGraphLaunch(h->graph_u, h->stream));
+            h->iter += kGraphUnroll;
+            it += kGraphUnroll;
+            continue;
+        }
         const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
         CUDA_TRY(h, cudaGraphLaunch(refresh ? h->graph_refresh : h->graph, h->stream));
         h->iter += 1;
+        ++it;
     }
     return SPFOM_OK;
 }
@@ -1624,14 +1703,34 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
     std::vector<cudaEvent_t> ev(2 * k + 1);
     for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
     spfom_status st = SPFOM_OK;
-    for (int64_t it = 0; it < k && st == SPFOM_OK; ++it) {
+    for (int64_t it = 0; it < k && st == SPFOM_OK;) {
+        if (h->graph_timed[1] && k - it >= kGraphUnroll) {
+            cudaError_t e = cudaSuccess;
+            for (int q = 0; q < 2 * kGraphUnroll && e == cudaSuccess; ++q)
+                e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[1], h->timed_node[1][q], ev[2 * it + q]);
+            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_timed[1], h->stream);
+            if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
+            h->iter += kGraphUnroll;
+            it += kGraphUnroll;
+            continue;
+        }
         const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
-        cudaError_t e = cudaEventRecord(ev[2 * it], h->stream);
-        if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_primal, h->stream);
-        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * it + 1], h->stream);
-        if (e == cudaSuccess) e = cudaGraphLaunch(refresh ? h->graph_rest_refresh : h->graph_rest, h->stream);
+        cudaError_t e = cudaSuccess;
+        if (refresh) {
+            // refresh iterations: the split form (events between two graphs)
+            e = cudaEventRecord(ev[2 * it], h->stream);
+            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_primal, h->stream);
+            if (e == cudaSuccess) e = cudaEventRecord(ev[2 * it + 1], h->stream);
+            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_rest_refresh, h->stream);
+        } else {
+            // one graph per iteration, as spfom_step: its event nodes record this iteration's pair
+            e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[0], h->timed_node[0][0], ev[2 * it]);
+            if (e == cudaSuccess) e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[0], h->timed_node[0][1], ev[2 * it + 1]);
+            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_timed[0], h->stream);
+        }
         if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
         h->iter += 1;
+        ++it;
     }
     if (st == SPFOM_OK && cudaEventRecord(ev[2 * k], h->stream) != cudaSuccess)
         st = fail(h, SPFOM_ECUDA, "spfom_step_timed: final event");
@@ -1769,8 +1868,14 @@ void spfom_destroy(spfom_handle *h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->graph_refresh) cudaGraphExecDestroy(h->graph_refresh);
-    for (cudaGraphExec_t g : {h->graph_primal, h->graph_rest, h->graph_rest_refresh})
+    for (cudaGraphExec_t g : {h->graph_u, h->graph_primal, h->graph_rest, h->graph_rest_refresh, h->graph_timed[0],
+                              h->graph_timed[1]})
         if (g) cudaGraphExecDestroy(g);
+    for (int u = 0; u < 2; ++u) {
+        if (h->graph_timed_src[u]) cudaGraphDestroy(h->graph_timed_src[u]);
+        for (cudaEvent_t e : h->timed_ev[u])
+            if (e) cudaEventDestroy(e);
+    }
     if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
     for (int b = 0; b < kNumBins; ++b) {
         if (h->side[b]) cudaStreamDestroy(h->side[b]);

@@ -431,6 +431,20 @@ __device__ __forceinline__ void flush_hists(const double *hist, int nh, int hs, 
 // groups falls in different banks
 __host__ __device__ constexpr int hist_stride(int HH) { return HH + 1; }
 
+// Dynamic round claims: work[0] is the claim counter of the launch, work[1]
+// counts exited blocks; the last block resets both for the next launch (so
+// the iteration graph needs no memset node before K1).
+__device__ __forceinline__ void release_work(unsigned long long *work) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+            work[0] = 0ull;
+            work[1] = 0ull;
+        }
+    }
+}
+
 // ============================================================== k_primal_stream
 // Full sweep over segments [first, first + count) of one bin (contiguous).
 #ifndef SPFOM_SPREAD_C
@@ -862,6 +876,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
         }
     }
+    if constexpr (CH > 0) release_work(L.work);
     __syncthreads();
     // flush: histogram h of warp w lives at w * PER_WARP + SLOT + h * HS
     {
@@ -1168,6 +1183,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
             if (st.restarts) atomicAdd(S.counters + 2, st.restarts);
         }
     }
+    if constexpr (CH > 0) release_work(L.work);
 }
 
 // ============================================================== k_primal (lists)
