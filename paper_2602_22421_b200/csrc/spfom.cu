@@ -251,11 +251,15 @@ struct spfom_handle {
     cudaGraphExec_t graph_primal = nullptr, graph_rest = nullptr, graph_rest_refresh = nullptr;   // split form (refresh iterations of spfom_step_timed)
     // timed form: the iteration graph with an event-record node before and after
     // the primal kernels; spfom_step_timed points them at fresh events per launch
-    // (timed_*[0]: one iteration, [1]: kGraphUnroll iterations)
-    cudaGraph_t graph_timed_src[2] = {nullptr, nullptr};
-    cudaGraphExec_t graph_timed[2] = {nullptr, nullptr};
-    std::vector<cudaGraphNode_t> timed_node[2];
-    std::vector<cudaEvent_t> timed_ev[2];
+    // timed form: c iterations in one graph, event-record nodes before and after
+    // the primal kernels of each and one after the last (events owned here);
+    // built on first use per chunk size c, kept for the handle's lifetime
+    struct TimedGraph {
+        int64_t iters = 0;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<cudaEvent_t> ev;   // [2 iters + 1]
+    };
+    std::vector<TimedGraph> timed;
     std::string err;
     int sm_count = 148;
     int device = 0;                            // every entry point runs with this device current
@@ -568,51 +572,66 @@ spfom_status build_graph(spfom_handle *h, bool refresh, cudaGraphExec_t *out, in
     return SPFOM_OK;
 }
 
-// The timed iteration graph (u = 0: one iteration, 1: kGraphUnroll): per
-// iteration, event record -> primal kernels -> event record -> the rest (no
-// refresh).  cudaEventRecordExternal makes the records event-record nodes (a
-// plain record inside a capture only orders streams).
-spfom_status build_timed_graph(spfom_handle *h, int u) {
-    const int iters = u ? kGraphUnroll : 1;
-    h->timed_ev[u].assign(2 * iters, nullptr);
-    h->timed_node[u].assign(2 * iters, nullptr);
-    for (auto &e : h->timed_ev[u]) CUDA_TRY(h, cudaEventCreate(&e));
-    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+// The timed graph of c iterations: per iteration, event record -> primal
+// kernels -> event record -> the rest (no refresh); a final event record.
+// cudaEventRecordExternal makes the records event-record nodes (a plain
+// record inside a capture only orders streams).  Its events are fixed, so a
+// launch needs no graph update.
+spfom_status timed_graph(spfom_handle *h, int64_t c, spfom_handle::TimedGraph **out) {
+    for (auto &tg : h->timed)
+        if (tg.iters == c) {
+            *out = &tg;
+            return SPFOM_OK;
+        }
+    spfom_handle::TimedGraph tg;
+    tg.iters = c;
+    tg.ev.assign(2 * c + 1, nullptr);
+    auto cleanup = [&]() {
+        for (cudaEvent_t e : tg.ev)
+            if (e) cudaEventDestroy(e);
+    };
+    for (auto &e : tg.ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            cleanup();
+            return fail(h, SPFOM_ECUDA, "timed graph: event create");
+        }
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cleanup();
+        return fail(h, SPFOM_ECUDA, "timed graph: begin capture");
+    }
     spfom_status st = SPFOM_OK;
-    for (int it = 0; it < iters && st == SPFOM_OK; ++it) {
-        if (cudaEventRecordWithFlags(h->timed_ev[u][2 * it], h->stream, cudaEventRecordExternal) != cudaSuccess)
+    auto rec = [&](cudaEvent_t e) {
+        if (st == SPFOM_OK && cudaEventRecordWithFlags(e, h->stream, cudaEventRecordExternal) != cudaSuccess)
             st = fail(h, SPFOM_ECUDA, "timed graph: event record");
+    };
+    for (int64_t it = 0; it < c && st == SPFOM_OK; ++it) {
+        rec(tg.ev[2 * it]);
         if (st == SPFOM_OK) st = enqueue_primal(h, nullptr);
-        if (st == SPFOM_OK &&
-            cudaEventRecordWithFlags(h->timed_ev[u][2 * it + 1], h->stream, cudaEventRecordExternal) != cudaSuccess)
-            st = fail(h, SPFOM_ECUDA, "timed graph: event record");
+        rec(tg.ev[2 * it + 1]);
         if (st == SPFOM_OK) st = enqueue_rest(h, false, nullptr);
     }
+    rec(tg.ev[2 * c]);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (st == SPFOM_OK && e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("timed graph capture: ") + cudaGetErrorString(e));
+    if (st == SPFOM_OK && cudaGraphInstantiate(&tg.exec, g, 0) != cudaSuccess) st = fail(h, SPFOM_ECUDA, "timed graph: instantiate");
+    if (g) cudaGraphDestroy(g);
     if (st != SPFOM_OK) {
-        if (g) cudaGraphDestroy(g);
+        cleanup();
         return st;
     }
-    if (e != cudaSuccess) return fail(h, SPFOM_ECUDA, std::string("timed graph capture: ") + cudaGetErrorString(e));
-    h->graph_timed_src[u] = g;
-    size_t nn = 0;
-    CUDA_TRY(h, cudaGraphGetNodes(g, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    CUDA_TRY(h, cudaGraphGetNodes(g, nodes.data(), &nn));
-    for (cudaGraphNode_t n : nodes) {
-        cudaGraphNodeType ty;
-        CUDA_TRY(h, cudaGraphNodeGetType(n, &ty));
-        if (ty != cudaGraphNodeTypeEventRecord) continue;
-        cudaEvent_t ev = nullptr;
-        CUDA_TRY(h, cudaGraphEventRecordNodeGetEvent(n, &ev));
-        for (int k = 0; k < 2 * iters; ++k)
-            if (ev == h->timed_ev[u][k]) h->timed_node[u][k] = n;
-    }
-    for (cudaGraphNode_t n : h->timed_node[u])
-        if (!n) return fail(h, SPFOM_ECUDA, "timed graph: event nodes not found");
-    CUDA_TRY(h, cudaGraphInstantiate(&h->graph_timed[u], g, 0));
+    h->timed.push_back(std::move(tg));
+    *out = &h->timed.back();
     return SPFOM_OK;
+}
+
+void destroy_timed(spfom_handle *h) {
+    for (auto &tg : h->timed) {
+        if (tg.exec) cudaGraphExecDestroy(tg.exec);
+        for (cudaEvent_t e : tg.ev)
+            if (e) cudaEventDestroy(e);
+    }
+    h->timed.clear();
 }
 
 // ------------------------------------------------------------------ device-resident instances
@@ -889,13 +908,9 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
         if (h->ev_fork) cudaEventDestroy(h->ev_fork);
         for (cudaGraphExec_t g : {h->graph, h->graph_u, h->graph_refresh, h->graph_primal, h->graph_rest,
-                                  h->graph_rest_refresh, h->graph_timed[0], h->graph_timed[1]})
+                                  h->graph_rest_refresh})
             if (g) cudaGraphExecDestroy(g);
-        for (int u = 0; u < 2; ++u) {
-            if (h->graph_timed_src[u]) cudaGraphDestroy(h->graph_timed_src[u]);
-            for (cudaEvent_t e : h->timed_ev[u])
-                if (e) cudaEventDestroy(e);
-        }
+        destroy_timed(h);
         for (int c = 0; c < 2; ++c) {
             if (h->pin_ev[c]) cudaEventSynchronize(h->pin_ev[c]);
             if (h->pin[c]) cudaFreeHost(h->pin[c]);
@@ -1271,12 +1286,12 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     ptimer.mark("H2D + state + modes");
     st = build_graph(h, false, &h->graph);
     if (st == SPFOM_OK && !(pl.sampled && p->refresh_every > 0)) st = build_graph(h, false, &h->graph_u, 0, kGraphUnroll);
-    if (st == SPFOM_OK) st = build_timed_graph(h, 0);
-    if (st == SPFOM_OK && h->graph_u) st = build_timed_graph(h, 1);
+
     if (st != SPFOM_OK) return bail(st);
     if (pl.sampled && p->refresh_every > 0) {
         st = build_graph(h, true, &h->graph_refresh);
         if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_primal, 1);
+        if (st == SPFOM_OK) st = build_graph(h, false, &h->graph_rest, 2);
         if (st == SPFOM_OK) st = build_graph(h, true, &h->graph_rest_refresh, 2);
         if (st != SPFOM_OK) return bail(st);
     }
@@ -1700,58 +1715,67 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms) {
         cudaEventDestroy(e1);
         return st;
     }
-    std::vector<cudaEvent_t> ev(2 * k + 1);
-    for (auto &e : ev) CUDA_TRY(h, cudaEventCreate(&e));
-    spfom_status st = SPFOM_OK;
-    for (int64_t it = 0; it < k && st == SPFOM_OK;) {
-        if (h->graph_timed[1] && k - it >= kGraphUnroll) {
-            cudaError_t e = cudaSuccess;
-            for (int q = 0; q < 2 * kGraphUnroll && e == cudaSuccess; ++q)
-                e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[1], h->timed_node[1][q], ev[2 * it + q]);
-            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_timed[1], h->stream);
-            if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
-            h->iter += kGraphUnroll;
-            it += kGraphUnroll;
-            continue;
-        }
-        const bool refresh = h->graph_refresh && ((h->iter + 1) % h->params.refresh_every == 0);
-        cudaError_t e = cudaSuccess;
-        if (refresh) {
-            // refresh iterations: the split form (events between two graphs)
-            e = cudaEventRecord(ev[2 * it], h->stream);
+    double primal = 0.0, total = 0.0;
+    if (h->graph_refresh) {
+        // sampled mode with periodic refreshes: iteration by iteration, events
+        // between the primal graph and the rest (plain or refresh) graph
+        std::vector<cudaEvent_t> ev(2 * k + 1, nullptr);
+        spfom_status st = SPFOM_OK;
+        for (auto &e : ev)
+            if (st == SPFOM_OK && cudaEventCreate(&e) != cudaSuccess) st = fail(h, SPFOM_ECUDA, "event create");
+        for (int64_t it = 0; it < k && st == SPFOM_OK; ++it) {
+            const bool refresh = (h->iter + 1) % h->params.refresh_every == 0;
+            cudaError_t e = cudaEventRecord(ev[2 * it], h->stream);
             if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_primal, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(ev[2 * it + 1], h->stream);
-            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_rest_refresh, h->stream);
-        } else {
-            // one graph per iteration, as spfom_step: its event nodes record this iteration's pair
-            e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[0], h->timed_node[0][0], ev[2 * it]);
-            if (e == cudaSuccess) e = cudaGraphExecEventRecordNodeSetEvent(h->graph_timed[0], h->timed_node[0][1], ev[2 * it + 1]);
-            if (e == cudaSuccess) e = cudaGraphLaunch(h->graph_timed[0], h->stream);
+            if (e == cudaSuccess) e = cudaGraphLaunch(refresh ? h->graph_rest_refresh : h->graph_rest, h->stream);
+            if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
+            h->iter += 1;
         }
-        if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed: ") + cudaGetErrorString(e));
-        h->iter += 1;
-        ++it;
+        if (st == SPFOM_OK && cudaEventRecord(ev[2 * k], h->stream) != cudaSuccess) st = fail(h, SPFOM_ECUDA, "final event");
+        if (st == SPFOM_OK) {
+            cudaError_t e = cudaEventSynchronize(ev[2 * k]);
+            for (int64_t it = 0; it < k && e == cudaSuccess; ++it) {
+                float a = 0.f;
+                e = cudaEventElapsedTime(&a, ev[2 * it], ev[2 * it + 1]);
+                primal += a;
+            }
+            float tt = 0.f;
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&tt, ev[0], ev[2 * k]);
+            total = tt;
+            if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed events: ") + cudaGetErrorString(e));
+        }
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        ms[0] = primal;
+        ms[1] = total;
+        return st;
     }
-    if (st == SPFOM_OK && cudaEventRecord(ev[2 * k], h->stream) != cudaSuccess)
-        st = fail(h, SPFOM_ECUDA, "spfom_step_timed: final event");
-    double primal = 0.0, total = 0.0;
-    if (st == SPFOM_OK) {
-        cudaError_t e = cudaEventSynchronize(ev[2 * k]);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-        for (int64_t it = 0; it < k && e == cudaSuccess; ++it) {
+    // chunks of up to kTimedChunk iterations, each one launch of a cached timed
+    // graph; the device times of the chunks add up (between chunks the host
+    // reads the events: a gap that is not counted)
+    constexpr int64_t kTimedChunk = 256;
+    for (int64_t done = 0; done < k;) {
+        const int64_t c = std::min(k - done, kTimedChunk);
+        spfom_handle::TimedGraph *tg = nullptr;
+        spfom_status st = timed_graph(h, c, &tg);
+        if (st != SPFOM_OK) return st;
+        CUDA_TRY(h, cudaGraphLaunch(tg->exec, h->stream));
+        CUDA_TRY(h, cudaEventSynchronize(tg->ev[2 * c]));
+        for (int64_t it = 0; it < c; ++it) {
             float a = 0.f;
-            e = cudaEventElapsedTime(&a, ev[2 * it], ev[2 * it + 1]);
+            CUDA_TRY(h, cudaEventElapsedTime(&a, tg->ev[2 * it], tg->ev[2 * it + 1]));
             primal += a;
         }
         float tt = 0.f;
-        if (e == cudaSuccess) e = cudaEventElapsedTime(&tt, ev[0], ev[2 * k]);
-        total = tt;
-        if (e != cudaSuccess) st = fail(h, SPFOM_ECUDA, std::string("spfom_step_timed events: ") + cudaGetErrorString(e));
+        CUDA_TRY(h, cudaEventElapsedTime(&tt, tg->ev[0], tg->ev[2 * c]));
+        total += tt;
+        h->iter += c;
+        done += c;
     }
-    for (auto &e : ev) cudaEventDestroy(e);
     ms[0] = primal;
     ms[1] = total;
-    return st;
+    return SPFOM_OK;
 }
 
 }   // extern "C" (templates below)
@@ -1868,14 +1892,9 @@ void spfom_destroy(spfom_handle *h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     if (h->graph_refresh) cudaGraphExecDestroy(h->graph_refresh);
-    for (cudaGraphExec_t g : {h->graph_u, h->graph_primal, h->graph_rest, h->graph_rest_refresh, h->graph_timed[0],
-                              h->graph_timed[1]})
+    for (cudaGraphExec_t g : {h->graph_u, h->graph_primal, h->graph_rest, h->graph_rest_refresh})
         if (g) cudaGraphExecDestroy(g);
-    for (int u = 0; u < 2; ++u) {
-        if (h->graph_timed_src[u]) cudaGraphDestroy(h->graph_timed_src[u]);
-        for (cudaEvent_t e : h->timed_ev[u])
-            if (e) cudaEventDestroy(e);
-    }
+    destroy_timed(h);
     if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
     for (int b = 0; b < kNumBins; ++b) {
         if (h->side[b]) cudaStreamDestroy(h->side[b]);

@@ -227,8 +227,11 @@ class Solver:
     def __init__(self, inst, params: Optional[Params] = None, *, device=None, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  segment_offset: int = 0, num_segments_global: Optional[int] = None,
-                 shared_periods: bool = True, workspace_offset_bytes: int = 0):
-        """workspace_offset_bytes > 0: a device allocation of that size is made
+                 shared_periods: bool = True, workspace_offset_bytes: int = 0, workspace=None):
+        """workspace: an optional caller-provided uint8 CUDA tensor of at least
+        workspace_bytes(inst, params) + 256 bytes (spfom_create's workspace
+        argument; the solver keeps a reference).
+        workspace_offset_bytes > 0: a device allocation of that size is made
         (and kept for the solver's lifetime) before the workspace, which then
         lands above it -- measured on B200, a workspace in the low part of
         device memory makes the primal kernel 0-15% slower, run to run
@@ -298,7 +301,13 @@ class Solver:
             self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
             self._placement_pad = (torch.empty(int(workspace_offset_bytes), dtype=torch.uint8, device=self.device)
                                    if workspace_offset_bytes > 0 else None)
-            self.workspace = torch.empty(max(int(nbytes.value), 256) + 256, dtype=torch.uint8, device=self.device)
+            need = max(int(nbytes.value), 256) + 256
+            if workspace is not None:
+                if not _is_cuda_tensor(workspace) or workspace.dtype != torch.uint8 or workspace.numel() < need:
+                    raise SpfomError(6, f"workspace: need a uint8 CUDA tensor of >= {need} bytes")
+                self.workspace = workspace
+            else:
+                self.workspace = torch.empty(need, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
         self._id = None
