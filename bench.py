@@ -25,10 +25,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # Eager CUDA module loading (read at CUDA initialisation, so before torch
-# touches the GPU).  Measured on B200: with the default lazy loading the
-# primal kernel K1 runs ~15% slower in a live loop than the same launch under
-# ncu or with eager loading (huge: 0.49 vs 0.42 ms; bench 1930 vs 2111 it/s);
-# DESIGN.md §9.  An explicit setting in the environment wins.
+# touches the GPU).  Measured on B200 (round 2): in the first iterations (the
+# bench window) K1 is the same with lazy and eager loading (0.444 ms), but
+# after ~1500 iterations it is 0.498 ms with lazy loading against 0.441 ms
+# eager (profiles/r02_placement.txt).  An explicit setting in the
+# environment wins.
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 METRIC = "SPFOM iterations/s (fp64, full sweep)"
@@ -380,10 +381,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     params = Params.converge()
-    # workspace above the first 32 GiB of device memory (placement
-    # in the low region makes K1 0-15% slower, run to run)
-    free_b, _total_b = torch.cuda.mem_get_info(device)
-    pad = (32 << 30) if free_b > (64 << 30) else 0
+    pad = 0   # no placement pad: the workspace offset does not change K1 (profiles/r02_placement.txt)
     kw = dict(device=device, rank=rank, world=world, nccl_id=nid, segment_offset=lo,
               num_segments_global=inst.m if T == 1 else int(inst.meta.get("m_per_period", inst.m // T)),
               shared_periods=not args.stacked, workspace_offset_bytes=pad)
