@@ -21,13 +21,21 @@ inventory (segments see no global scarcity), then applies the sales
 segment by segment to the shared inventory.
 
 This module is an application of the library (the optimisation runs in the
-CUDA kernels); the per-customer choice sampling is host bookkeeping.
+CUDA kernels); the per-customer choice sampling is host bookkeeping.  The
+dual solve is a parameter (`solve`, default: the GPU path through `Solver`),
+so the same trace can be replayed with another solver's duals -- the tests
+replay it with the CPU oracle's.
+
+`bid_price_control` is the bid-price rule itself (offer j iff
+r_j - eta_j >= 0) applied to the customers of a multi-period SBLP instance
+(BASELINE config 5: "SPFOM duals used as bid prices") with one shared
+inventory.
 """
 from __future__ import annotations
 
 import dataclasses
 import math
-from typing import List, Optional
+from typing import Callable, List, Optional
 
 import numpy as np
 
@@ -55,6 +63,7 @@ class SimTrace:
     inventory: np.ndarray                 # [batches + 1, products] (row 0 = initial)
     duals: List[Optional[np.ndarray]]     # per batch: bid prices used (None = no solve), per segment for MSD
     solves: int
+    offered: Optional[List] = None        # per batch: product mask of what was recommended (per segment for MSD)
 
     @property
     def cumulative_revenue(self) -> np.ndarray:
@@ -85,23 +94,31 @@ def market(cfg: SimConfig):
     return prices, inventory, prefs
 
 
+def gpu_solve(inst, iters: int) -> np.ndarray:
+    """The default dual solve: `iters` SPFOM iterations (converge preset) on the GPU."""
+    s = Solver(inst, Params.converge())
+    s.step(iters)
+    eta = s.duals()
+    s.close()
+    return eta
+
+
 def _bid_prices(prefs: np.ndarray, avail: np.ndarray, prices: np.ndarray, inventory: np.ndarray,
-                cfg: SimConfig, horizon: int) -> np.ndarray:
+                cfg: SimConfig, horizon: int, solve: Callable) -> np.ndarray:
     """SBLP of one customer group (arrival = remaining batches each, reading
     c18; consideration set = `avail`; capacities = remaining inventory) solved
-    by SPFOM on the GPU; returns eta over all products (0 off `avail`)."""
+    by `solve(instance, iters)`; returns eta over all products (0 off `avail`)."""
     n, k = prefs.shape[0], int(avail.size)
     seg_ptr = np.arange(n + 1, dtype=np.int64) * k
     prod = np.tile(avail.astype(np.int32), n)
     v = np.maximum(prefs[:, avail].reshape(-1), 1e-9)           # attraction > 0 (U[0,1] draws)
+    present = np.zeros(prices.shape[0], dtype=bool)
+    present[avail] = True
     inst = _BatchInstance(seg_ptr=seg_ptr, prod_idx=prod, attract=v, shadow=np.zeros_like(v),
                           no_purchase=np.full(n, cfg.no_purchase), arrival=np.full(n, float(horizon)),
-                          price=np.asarray(prices, float), capacity=np.asarray(inventory, float))
-    s = Solver(inst, Params.converge())
-    s.step(cfg.iters)
-    eta = s.duals()
-    s.close()
-    return eta
+                          price=np.asarray(prices, float), capacity=np.asarray(inventory, float),
+                          meta=dict(present=present))
+    return solve(inst, cfg.iters)
 
 
 def _recommend(prefs: np.ndarray, avail: np.ndarray, margin: np.ndarray, K: int) -> np.ndarray:
@@ -141,7 +158,8 @@ def _purchase(prefs: np.ndarray, offer: np.ndarray, inventory: np.ndarray, price
     return rev, sold
 
 
-def _run(cfg: SimConfig, segments: int) -> SimTrace:
+def _run(cfg: SimConfig, segments: int, solve: Optional[Callable] = None) -> SimTrace:
+    solve = solve or gpu_solve
     prices, inv0, prefs_all = market(cfg)
     rng = np.random.default_rng(np.random.SeedSequence([cfg.seed, 777]))
     inventory = inv0.copy()
@@ -150,6 +168,7 @@ def _run(cfg: SimConfig, segments: int) -> SimTrace:
     inv_trace = np.zeros((B + 1, m))
     inv_trace[0] = inventory
     duals: List[Optional[np.ndarray]] = []
+    offered: List = []
     solves = 0
     for b in range(B):
         prefs = prefs_all[b]
@@ -165,7 +184,7 @@ def _run(cfg: SimConfig, segments: int) -> SimTrace:
                 offer[:, avail] = True
                 batch_duals.append(None)
             else:
-                eta = _bid_prices(prefs[gidx], avail, prices, inventory, cfg, B - b)
+                eta = _bid_prices(prefs[gidx], avail, prices, inventory, cfg, B - b, solve)
                 solves += 1
                 batch_duals.append(eta)
                 offer = _recommend(prefs[gidx], avail, prices - eta, cfg.rec_limit)
@@ -180,17 +199,19 @@ def _run(cfg: SimConfig, segments: int) -> SimTrace:
         revenue[b], sold[b] = rev_b, sold_b
         inv_trace[b + 1] = inventory
         duals.append(batch_duals[0] if segments == 1 else batch_duals)
-    return SimTrace(revenue=revenue, sold=sold, inventory=inv_trace, duals=duals, solves=solves)
+        masks = [o.any(axis=0) for o in offers]
+        offered.append(masks[0] if segments == 1 else masks)
+    return SimTrace(revenue=revenue, sold=sold, inventory=inv_trace, duals=duals, solves=solves, offered=offered)
 
 
-def run_go_policy(cfg: SimConfig) -> SimTrace:
+def run_go_policy(cfg: SimConfig, solve: Optional[Callable] = None) -> SimTrace:
     """GO: one SBLP per batch over all its customers."""
-    return _run(cfg, 1)
+    return _run(cfg, 1, solve)
 
 
-def run_msd_policy(cfg: SimConfig) -> SimTrace:
+def run_msd_policy(cfg: SimConfig, solve: Optional[Callable] = None) -> SimTrace:
     """MSD: `cfg.segments` round-robin groups, each with its own SBLP."""
-    return _run(cfg, cfg.segments)
+    return _run(cfg, cfg.segments, solve)
 
 
 def sales_entropy(sold_total: np.ndarray) -> float:
@@ -204,15 +225,84 @@ def sales_entropy(sold_total: np.ndarray) -> float:
 
 
 def mean_opportunity_cost(trace: SimTrace) -> float:
-    """Average bid price over (batch, product in stock) pairs where a solve occurred."""
+    """Average bid price over the (batch, recommended product) pairs of the
+    batches with a solve (the opportunity cost of what was
+    offered; per segment for MSD)."""
     vals = []
     for b, d in enumerate(trace.duals):
         ds = d if isinstance(d, list) else [d]
-        inv = trace.inventory[b]
-        for e in ds:
+        ms = trace.offered[b] if isinstance(trace.offered[b], list) else [trace.offered[b]]
+        for e, mask in zip(ds, ms):
             if e is not None:
-                vals.extend(np.asarray(e)[inv >= 1.0].tolist())
+                vals.extend(np.asarray(e)[mask].tolist())
     return float(np.mean(vals)) if vals else 0.0
+
+
+@dataclasses.dataclass
+class BidPriceTrace:
+    revenue: np.ndarray                   # [periods]
+    sold: np.ndarray                      # [periods, products]
+    inventory: np.ndarray                 # [periods + 1, products] (row 0 = capacity)
+    offers: int                           # customers shown at least one product
+    min_margin: float                     # smallest |r_j - eta_j| among offered products (ties)
+
+
+def bid_price_control(inst, eta: np.ndarray, customers_per_period: int, rec_limit: int = 2,
+                      seed: int = 0) -> BidPriceTrace:
+    """The bid-price rule on a multi-period instance (reading
+    c15 stacking, config 5): the converged duals eta_j price the one shared
+    inventory c_j.  In period t, customers arrive from base segment i with
+    probability proportional to lambda_{i,t}; a customer is shown the top
+    `rec_limit` products of C_i in stock with r_j - eta_j >= 0, ranked by
+    (r_j - eta_j) v_ij, and buys under GAM: product j of the
+    shown set S with probability v_ij / (v_i0 + sum_S v + sum_{C_i \\ S} w);
+    a sale takes one unit of inventory.  Seeded draws; host bookkeeping."""
+    T = int((getattr(inst, "meta", None) or {}).get("T", 1) or 1)
+    M = int(inst.seg_ptr.shape[0] - 1)
+    m = M // T
+    nb = int(inst.seg_ptr[m])
+    seg_ptr = np.asarray(inst.seg_ptr[: m + 1])
+    prod, v = np.asarray(inst.prod_idx[:nb]), np.asarray(inst.attract[:nb])
+    w = np.asarray(inst.shadow[:nb]) if getattr(inst, "shadow", None) is not None else np.zeros(nb)
+    v0 = np.asarray(inst.no_purchase[:m])
+    lam = np.asarray(inst.arrival, float).reshape(T, m)
+    r = np.asarray(inst.price, float)
+    margin = r - np.asarray(eta, float)
+    inventory = np.floor(np.asarray(inst.capacity, float))
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 515]))
+    revenue, sold = np.zeros(T), np.zeros((T, r.shape[0]))
+    inv_trace = np.zeros((T + 1, r.shape[0]))
+    inv_trace[0] = inventory
+    offers, min_margin = 0, np.inf
+    for t in range(T):
+        p = lam[t] / lam[t].sum()
+        segs = rng.choice(m, size=customers_per_period, p=p)
+        u = rng.uniform(0.0, 1.0, customers_per_period)
+        for c in range(customers_per_period):
+            i = int(segs[c])
+            a, b = int(seg_ptr[i]), int(seg_ptr[i + 1])
+            js, vi, wi = prod[a:b], v[a:b], w[a:b]
+            ok = (margin[js] >= 0.0) & (inventory[js] >= 1.0)
+            if not ok.any():
+                continue
+            score = np.where(ok, margin[js] * vi, -np.inf)
+            top = np.argsort(-score, kind="stable")[: min(rec_limit, int(ok.sum()))]
+            top = top[np.isfinite(score[top])]
+            offers += 1
+            min_margin = min(min_margin, float(np.abs(margin[js[top]]).min()))
+            shown = np.zeros(b - a, dtype=bool)
+            shown[top] = True
+            den = v0[i] + vi[shown].sum() + wi[~shown].sum()
+            cum = np.cumsum(vi[top]) / den
+            k = int(np.searchsorted(cum, u[c], side="right"))
+            if k < top.size:
+                j = int(js[top[k]])
+                inventory[j] -= 1.0
+                sold[t, j] += 1.0
+                revenue[t] += r[j]
+        inv_trace[t + 1] = inventory
+    return BidPriceTrace(revenue=revenue, sold=sold, inventory=inv_trace, offers=offers,
+                         min_margin=float(min_margin))
 
 
 def cumulative_revenue_identity(trace: SimTrace, prices: np.ndarray) -> float:
