@@ -1367,9 +1367,15 @@ spfom_status spfom_step(spfom_handle *h, int64_t k) {
 }
 
 static spfom_status check_counters(spfom_handle *h) {
-    unsigned long long cnt[3];
+    unsigned long long cnt[6];
     CUDA_TRY(h, cudaMemcpyAsync(cnt, h->S.counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (cnt[5] != 0) {   // SPFOM_DEVICE_CHECKS builds only
+        char buf[128];
+        snprintf(buf, sizeof buf, "device index / size checks failed %llu times", cnt[5]);
+        h->err = buf;
+        return SPFOM_ENUMERIC;
+    }
     if (cnt[0] != 0) {
         char buf[128];
         snprintf(buf, sizeof buf, "projection hit max_newton on %llu segment-iterations", cnt[0]);

@@ -64,6 +64,17 @@ struct DevState {
     int32_t sampled;               // 1 => scatter y_new - y_old into s (stale rows kept)
 };
 
+// ----------------------------------------------------------------- device checks
+// SPFOM_DEVICE_CHECKS (debug build, tests/test_device_checks.py): index and
+// size checks in the primal kernels; a failed check increments counters[5]
+// (the next synchronising getter returns SPFOM_ENUMERIC) instead of trapping.
+// compute-sanitizer is closed on this GPU pool; this is its stand-in.
+#ifdef SPFOM_DEVICE_CHECKS
+#define SPFOM_DCHECK(S, cond) do { if (!(cond)) atomicAdd((S).counters + 5, 1ull); } while (0)
+#else
+#define SPFOM_DCHECK(S, cond) do { } while (0)
+#endif
+
 // ----------------------------------------------------------------- memory helpers
 __device__ __forceinline__ void ld256_nc(const double *p, double &a, double &b, double &c, double &d) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"

@@ -623,6 +623,8 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
         const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;        // window of round rw
+        SPFOM_DCHECK(S, qb >= qa && nq <= (uint32_t)LY::QMAX && qa >= 0 && (int64_t)qb <= S.nq * S.T);
+        SPFOM_DCHECK(S, left > 0 && s0 + n <= S.m);
         const uint32_t wbytes = (rw >= 0 && !uni) ? 4u * LY::QW : 0u;
         // one elected lane, straight-line: the copies take uniform operands
         if (lane == 0) {
@@ -763,6 +765,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         if (q1 >= 0) issue(q1, qn, q2);
         PH_MARK(8);
 
+#ifdef SPFOM_DEVICE_CHECKS
+#pragma unroll
+        for (int e = 0; e < NE; ++e) SPFOM_DCHECK(S, idx[e] >= 0 && idx[e] <= N);
+        SPFOM_DCHECK(S, qb - qa <= (EQ > 0 ? EQ : G * Q) && qa >= base && qb - base <= LY::QMAX);
+#endif
         // a2: price gather (g[N] = 0 for pads; head from shared memory).  The
         // opaque copies keep the two bases in registers (otherwise ptxas
         // rebuilds the shared window base and reloads S.g for every entry).
@@ -798,6 +805,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         if constexpr (EQ > 0) {
             // the group's 4 lanes write each quad's 32-B sector
             double *yp = S.y + 4 * (int64_t)qa + gl;
+            SPFOM_DCHECK(S, !active || (int64_t)qb <= S.nq);
             if (L.uni && left >= GPW) {
 #pragma unroll
                 for (int t = 0; t < EQ; ++t) yp[4 * t] = yv[t];
@@ -841,6 +849,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         for (int e = 0; e < NE; ++e) {
             const int j = idx[e];
             const int off = j < spread_n ? spread_rel + j : j;     // warm head -> this warp's spread copy
+            SPFOM_DCHECK(S, off >= 0 && off < S.spread_off + S.spread_c * spread_n);
             red_add_if(S.s + off, yv[e], j >= SPFOM_DIAG_RED_FROM && j < N && yv[e] != 0.0);
         }
 #endif
@@ -1020,6 +1029,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
         const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
         const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;
+        SPFOM_DCHECK(S, qb >= qa && nq <= (uint32_t)LY::QMAX && (int64_t)qb <= S.nq);
         const uint32_t wbytes = rw >= 0 ? 4u * LY::QW : 0u;
         if (lane == 0) {
             mbar_arrive_expect_tx(barS, 80u * nq + wbytes);
