@@ -175,6 +175,15 @@ typedef struct {
  * nccl_id == NULL (or no spfom_dist at all) => single GPU; world == 1 with an
  * id runs the multi-rank code path (NCCL allreduce of the usage, k_fold) on
  * one GPU with identical results -- a way to exercise it without peers. */
+/* Per iteration with world > 1 (products, no bundles), inside the CUDA graph:
+ * K1's usage partials -> ncclReduceScatter (rank r gets the summed usage of
+ * products [r c, (r + 1) c), c = ceil((N + 1) / world)) -> the Eq. 17 dual step
+ * on that slice only -> ncclAllGather of the prices g = r - eta.  eta and the
+ * usage stay sliced between iterations; spfom_duals / spfom_usage /
+ * spfom_averages / spfom_residuals gather them first (they are collective).
+ * Bundles (num_resources > 0), or the environment variable
+ * SPFOM_COLLECTIVE=allreduce at create, use ncclAllReduce of the usage and the
+ * dual step on every rank instead.  world <= 64. */
 typedef struct {
     int32_t rank;
     int32_t world;

@@ -41,6 +41,8 @@ struct NcclApi {
     nccl_res (*GetUniqueId)(nccl_uid *) = nullptr;
     nccl_res (*CommInitRank)(nccl_comm *, int, nccl_uid, int) = nullptr;
     nccl_res (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    nccl_res (*ReduceScatter)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    nccl_res (*AllGather)(const void *, void *, size_t, int, nccl_comm, cudaStream_t) = nullptr;
     nccl_res (*CommDestroy)(nccl_comm) = nullptr;
     const char *(*GetErrorString)(nccl_res) = nullptr;
 };
@@ -55,8 +57,11 @@ NcclApi &nccl() {
         api.CommInitRank = (nccl_res(*)(nccl_comm *, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
         api.AllReduce = (nccl_res(*)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
         api.CommDestroy = (nccl_res(*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+        api.ReduceScatter = (nccl_res(*)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclReduceScatter");
+        api.AllGather = (nccl_res(*)(const void *, void *, size_t, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllGather");
         api.GetErrorString = (const char *(*)(nccl_res))dlsym(h, "ncclGetErrorString");
-        api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+        api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.ReduceScatter &&
+                 api.AllGather;
     });
     return api;
 }
@@ -156,7 +161,12 @@ constexpr int kSpreadCopies = SPFOM_SPREAD_C;
 #define SPFOM_SPREAD_N 16384
 #endif
 int64_t spread_range(int64_t N) { return kSpreadCopies > 0 ? std::min<int64_t>(N, SPFOM_SPREAD_N) : 0; }
-int64_t spread_off(int64_t N) { return (N + 1 + 31) / 32 * 32; }   // first spread slot after the N + 1 acc slots
+// Product vectors hold N + 1 slots (slot N: the pads' dummy product) plus
+// kRankPad, so that with world P <= kRankPad the padded length round_up(N + 1,
+// P) that ReduceScatter / AllGather split into P equal slices fits.
+constexpr int64_t kRankPad = 64;
+int64_t prod_slots(int64_t N) { return N + 1 + kRankPad; }
+int64_t spread_off(int64_t N) { return (prod_slots(N) + 31) / 32 * 32; }   // first spread slot after the acc slots
 
 // pinned staging ring of a handle: 2 buffers of kPinQuads quads x 80 B (ids +
 // v + omega at create; the getters' D2H uses 32 B per quad of it)
@@ -180,7 +190,7 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     pl.sampled = p && p->blocks != nullptr;
     pl.averaging = p && p->averaging;
     pl.block_entries = pl.sampled ? p->block_iters * p->block_size : 0;
-    const int64_t nq = std::max<int64_t>(pl.nq, 1), m = std::max<int64_t>(pl.m, 1), N1 = pl.N + 1, T = pl.T;
+    const int64_t nq = std::max<int64_t>(pl.nq, 1), m = std::max<int64_t>(pl.m, 1), N1 = prod_slots(pl.N), T = pl.T;
     size_t sz[O_NSLOTS] = {0};
     sz[O_PIDX] = nq * 16;
     sz[O_V] = sz[O_OM] = nq * 32;
@@ -262,6 +272,10 @@ struct spfom_handle {
     std::vector<TimedGraph> timed;
     std::string err;
     int sm_count = 148;
+    // world > 1 (plain products): ReduceScatter -> K3 on the slice -> AllGather
+    // of g; the product vectors are split into world slices of `chunk`
+    bool rs = false;
+    int64_t chunk = 0, np = 0;
     int device = 0;                            // every entry point runs with this device current
     bool own_stream = false;
     // full sweep with several non-empty bins: one side stream per bin, SM share per bin
@@ -296,6 +310,15 @@ spfom_status allreduce(spfom_handle *h, const void *src, void *dst, size_t n, in
     }
     nccl_res r = nccl().AllReduce(src, dst, n, dtype, op, h->comm, h->stream);
     if (r != 0) return fail(h, SPFOM_ENCCL, std::string("ncclAllReduce: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
+    return SPFOM_OK;
+}
+
+// rs mode: make a sliced product vector (eta, s_prev, etabar) whole on every
+// rank (collective; in place)
+spfom_status gather_slices(spfom_handle *h, double *v) {
+    if (!h->rs) return SPFOM_OK;
+    nccl_res r = nccl().AllGather(v + h->rank * h->chunk, v, (size_t)h->chunk, kNcclFloat64, h->comm, h->stream);
+    if (r != 0) return fail(h, SPFOM_ENCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(r));
     return SPFOM_OK;
 }
 
@@ -525,6 +548,23 @@ spfom_status enqueue_rest(spfom_handle *h, bool refresh, int64_t *launches) {
         // fold the spread copies into acc before the cross-rank sum
         k_fold<<<std::max<int64_t>(1, (S.spread_n + kThreads - 1) / kThreads), kThreads, 0, h->stream>>>(S);
         ++nl;
+    }
+    if (h->rs) {
+        // a6 + a7 split over the ranks: sum only this rank's slice of the usage,
+        // update its duals, share the prices
+        const int64_t lo = h->rank * h->chunk;
+        nccl_res r = nccl().ReduceScatter(acc, acc + lo, (size_t)h->chunk, kNcclFloat64, kNcclSum, h->comm, h->stream);
+        if (r != 0) return fail(h, SPFOM_ENCCL, std::string("ncclReduceScatter: ") + nccl().GetErrorString(r));
+        const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((h->np + kThreads - 1) / kThreads, h->sm_count * 8));
+        k_dual_slice<<<gs, kThreads, 0, h->stream>>>(S, full_mode, h->pl.averaging ? 0 : 1, lo, h->chunk, h->np);
+        r = nccl().AllGather(S.g + lo, S.g, (size_t)h->chunk, kNcclFloat64, h->comm, h->stream);
+        if (r != 0) return fail(h, SPFOM_ENCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(r));
+        if (h->pl.averaging) k_average<<<h->sm_count * 8, kThreads, 0, h->stream>>>(S, h->T * h->nq);
+        if (h->pl.averaging) k_tick<<<1, 1, 0, h->stream>>>(S.t);
+        nl += 1 + (h->pl.averaging ? 2 : 0);
+        CUDA_TRY(h, cudaGetLastError());
+        if (launches) *launches = nl;
+        return SPFOM_OK;
     }
     spfom_status st = allreduce(h, acc, acc, (size_t)h->N, kNcclFloat64, kNcclSum);
     if (st != SPFOM_OK) return st;
@@ -1175,7 +1215,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
              H2D(O_RPTR, rptr_d.data(), (L + 1) * 4) && H2D(O_RBUN, rbun_d.data(), rbun_d.size() * 4);
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
-    ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, D1 * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, (N + 1) * 8) &&
+    ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, std::max<int64_t>(D1, prod_slots(N)) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, prod_slots(N) * 8) &&
          Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 16 * kNumBins);
     if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, D1 * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
@@ -1208,6 +1248,16 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.spread_n = (int32_t)spread_range(N);
     S.spread_c = kSpreadCopies;
     S.fold_in_dual = h->comm ? 0 : 1;
+    // world > 1 with plain products: ReduceScatter -> K3 on the slice ->
+    // AllGather (SPFOM_COLLECTIVE=allreduce keeps the allreduce + replicated K3)
+    {
+        const char *coll = getenv("SPFOM_COLLECTIVE");
+        h->rs = h->comm && L == 0 && h->world <= kRankPad && !(coll && strcmp(coll, "allreduce") == 0);
+        if (h->rs) {
+            h->chunk = (N + 1 + h->world - 1) / h->world;
+            h->np = h->chunk * h->world;
+        }
+    }
     S.s_prev = slot_ptr<double>(h, O_SCUR);
     S.etabar = pl.averaging ? slot_ptr<double>(h, O_ETABAR) : nullptr;
     S.counters = slot_ptr<unsigned long long>(h, O_COUNTERS);
@@ -1402,6 +1452,7 @@ static spfom_status fetch_duals(spfom_handle *h, const double *src, double *eta)
 spfom_status spfom_duals(spfom_handle *h, double *eta) {
     if (!h || !eta) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
+    if (spfom_status gs = gather_slices(h, h->S.eta); gs != SPFOM_OK) return gs;
     spfom_status st = fetch_duals(h, h->S.eta, eta);
     return st != SPFOM_OK ? st : check_counters(h);
 }
@@ -1409,6 +1460,7 @@ spfom_status spfom_duals(spfom_handle *h, double *eta) {
 spfom_status spfom_usage(spfom_handle *h, double *s) {
     if (!h || !s) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
+    if (spfom_status gs = gather_slices(h, h->S.s_prev); gs != SPFOM_OK) return gs;
     std::vector<double> tmp(h->N);
     CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->S.s_prev, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1490,6 +1542,7 @@ spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double
     if (!h) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
     if (!h->pl.averaging) return fail(h, SPFOM_EINVAL, "averaging is off");
+    if (spfom_status gs = gather_slices(h, h->S.etabar); gs != SPFOM_OK) return gs;
     spfom_status st = fetch_primal(h, h->S.ybar, h->S.y0bar, 8, ybar, y0bar);
     if (st != SPFOM_OK) return st;
     if (etabar) return fetch_duals(h, h->S.etabar, etabar);
@@ -1499,6 +1552,7 @@ spfom_status spfom_averages(spfom_handle *h, double *ybar, double *y0bar, double
 spfom_status spfom_residuals(spfom_handle *h, spfom_residuals_t *out) {
     if (!h || !out) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
+    if (spfom_status gs = gather_slices(h, h->S.eta); gs != SPFOM_OK) return gs;
     DevState S = h->S;
     double *sf = slot_ptr<double>(h, O_TMP);
     CUDA_TRY(h, cudaMemsetAsync(sf, 0, (h->N + 1) * 8, h->stream));

@@ -72,6 +72,29 @@ __global__ void __launch_bounds__(kThreads) k_dual(DevState S, int32_t full, int
     if (tick) tick_once(S);
 }
 
+// K3 on this rank's slice (world > 1, ReduceScatter -> K3 -> AllGather): the
+// ReduceScatter left the summed usage of products [lo, lo + chunk) in
+// acc[lo .. lo + chunk); this rank updates their eta, s_prev (and etabar)
+// and prices g (slots >= N: g = 0, the pads' dummy); the AllGather that follows
+// shares g.  eta / s_prev stay sliced (the getters gather them).  Every acc
+// slot of the padded length np is cleared for the next scatter.
+__global__ void __launch_bounds__(kThreads) k_dual_slice(DevState S, int32_t full, int32_t tick, int64_t lo,
+                                                         int64_t chunk, int64_t np) {
+    const int64_t t_next = tick ? 0 : *S.t + 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lo + chunk; j += stride) {
+        if (j < S.N) {
+            dual_update(S, j, full, t_next);
+        } else {
+            S.g[j] = 0.0;
+            S.s[j] = 0.0;
+        }
+    }
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += stride)
+        if (j < lo || j >= lo + chunk) S.s[j] = 0.0;
+    if (tick) tick_once(S);
+}
+
 // ----------------------------------------------------------------- bundles (a7, NRM)
 // P:L719-741 Eq. 33: the dual step runs over the L resources.
 // 1) per bundle: s_new, st = s_new + omega_x (s_new - s_prev), s_prev = s_new

@@ -4,7 +4,9 @@ The N > 1 path (Alg. 3): each rank owns a contiguous
 segment range from spfom_partition (the C library's host function), the
 per-product step sizes tau_j = 0.9 / n_j use GLOBAL column counts (allreduced
 once at create), and every iteration allreduces the usage vector before an
-identical dual step on every rank.  Here the ranks' primal steps are emulated
+identical dual step on every rank -- or (variant "rs", the library's default
+for world > 1) each rank updates the duals of its slice of the products and
+the slices are all-gathered.  Here the ranks' primal steps are emulated
 with the CPU oracle; the test checks partition invariance against the single-
 process oracle and that the ranks' duals are bitwise identical.
 """
@@ -70,10 +72,26 @@ def _worker(rank, world, port, errq, variant="plain"):
         ref = oracle.OracleSolver(inst)
         ent = np.concatenate([np.arange(inst.seg_ptr[a], inst.seg_ptr[b]) for a, b in rows])
         seg = np.concatenate([np.arange(a, b) for a, b in rows])
+        N = inst.N
+        chunk = (N + 1 + world - 1) // world          # spfom.cu: h->chunk (ReduceScatter slices)
+        plo = rank * chunk
         for _t in range(40):
             s = torch.from_numpy(S.primal_shard())
             dist.all_reduce(s)
-            S.dual_apply(s.numpy())
+            if variant == "rs":
+                # ReduceScatter -> dual step on this rank's slice -> AllGather
+                # (the library's default for world > 1; gloo has no
+                # reduce_scatter, so the slice is cut from the allreduce)
+                sl = slice(min(plo, N), min(plo + chunk, N))
+                new = oracle.dual_step(S.eta[sl], s.numpy()[sl], S.s[sl], inst.capacity[sl], tau[sl], 0.0, 1.0)
+                mine = torch.zeros(chunk, dtype=torch.float64)
+                mine[: new.shape[0]] = torch.from_numpy(new)
+                parts = [torch.zeros(chunk, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, mine)
+                S.eta[:] = torch.cat(parts).numpy()[:N]
+                S.s[:] = s.numpy()
+            else:
+                S.dual_apply(s.numpy())
             ref.step()
             scale = max(float(np.abs(ref.eta).max()), 1e-300)
             assert np.abs(S.eta - ref.eta).max() <= 1e-12 * max(scale, 1.0), "eta drifted from single-rank run"
@@ -92,7 +110,8 @@ def _worker(rank, world, port, errq, variant="plain"):
         raise
 
 
-@pytest.mark.parametrize("world,variant", [(2, "plain"), (3, "plain"), (2, "bundles"), (3, "multi")])
+@pytest.mark.parametrize("world,variant", [(2, "plain"), (3, "plain"), (2, "bundles"), (3, "multi"), (2, "rs"),
+                                           (3, "rs")])
 def test_sharded_iteration_matches_single_rank(world, variant):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()

@@ -116,7 +116,7 @@ def test_entry_mapped_bin_lockstep(preset, k):
     rounds, so the throughput mapping runs, not the wide latency one."""
     inst = generate("huge", m=24000 + 5, N=3000, k=k)
     p = _params(exec_mode=1) if preset == "converge" else _paper(mu=0.5, exec_mode=1)
-    worst, gpu, _ = lockstep(inst, p, 30)
+    worst, gpu, _ = lockstep(inst, p, 100, check_every=5, check_first=5)
     gpu.close()
     _assert_ok(worst)
 
@@ -550,33 +550,43 @@ def test_feature_combinations_lockstep(combo):
     _assert_ok(worst)
 
 
+@pytest.mark.parametrize("collective", ["reduce_scatter", "allreduce"])
 @pytest.mark.parametrize("name,kw", [("medium", dict(m=30000, N=4000, k=(20, 200))),
                                      ("multi", dict(m=3000, N=800, k=50, T=3))])
-def test_nccl_path_single_rank(name, kw):
+def test_nccl_path_single_rank(name, kw, collective, monkeypatch):
     """The multi-rank code path (ncclCommInitRank from a unique id, k_fold of the
-    spread copies, ncclAllReduce of the usage inside the CUDA graph, global
-    column counts by allreduce) run with world == 1 on this GPU: iterates equal
-    to the single-GPU path up to the order of the fp64 reductions (K1's global
-    RED order is not fixed, so two runs are not bitwise equal) and within
-    1e-10 of the oracle."""
+    spread copies, global column counts by allreduce, and per iteration either
+    ReduceScatter -> K3 on the rank's slice -> AllGather of the prices (the
+    default for world > 1) or an allreduce + replicated K3
+    (SPFOM_COLLECTIVE=allreduce), inside the CUDA graph), run with world == 1
+    on this GPU for 100 iterations: iterates equal to the single-GPU path up
+    to the order of the fp64 reductions (K1's global RED order is not fixed, so
+    two runs are not bitwise equal) and within 1e-10 of the oracle every 10
+    iterations; the getters gather the sliced duals / usage."""
     from paper_2602_22421_b200 import Params, Solver, nccl_unique_id
+    if collective == "allreduce":
+        monkeypatch.setenv("SPFOM_COLLECTIVE", "allreduce")
     inst = generate(name, **kw)
     p = Params.converge(exec_mode=1)
     a = Solver(inst, p)
     b = Solver(inst, p, rank=0, world=1, nccl_id=nccl_unique_id())
     assert b.info()["launches_per_iteration"] == a.info()["launches_per_iteration"] + 1   # + k_fold
     cpu = oracle.OracleSolver(inst, **oracle_kwargs(p))
-    for _ in range(20):
+    lam, rmax = float(inst.arrival.max()), float(inst.price.max())
+    for t in range(100):
         a.step(1)
         b.step(1)
         cpu.step()
+        if (t + 1) % 10 == 0:
+            yb, y0b = b.primal()
+            assert rel_inf(yb, cpu.y, lam) <= TOL_ITER and rel_inf(b.duals(), cpu.eta, rmax) <= TOL_ITER, t
+            assert rel_inf(b.usage(), cpu.s, lam) <= TOL_ITER
     ya, y0a = a.primal()
     yb, y0b = b.primal()
-    lam, rmax = float(inst.arrival.max()), float(inst.price.max())
     assert rel_inf(yb, ya, lam) <= 1e-12 and rel_inf(y0b, y0a, lam) <= 1e-12
     assert rel_inf(b.duals(), a.duals(), rmax) <= 1e-12
-    assert rel_inf(yb, cpu.y, lam) <= TOL_ITER and rel_inf(b.duals(), cpu.eta, rmax) <= TOL_ITER
     ra, rb = a.residuals(), b.residuals()
     assert abs(ra["primal_obj"] - rb["primal_obj"]) <= 1e-12 * abs(ra["primal_obj"])
+    assert abs(ra["dual_obj"] - rb["dual_obj"]) <= 1e-12 * abs(ra["dual_obj"])
     a.close()
     b.close()
