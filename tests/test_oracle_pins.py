@@ -508,3 +508,74 @@ def test_sales_entropy_examples():
     assert sales_entropy(np.array([0, 7, 0])) == 0.0
     assert abs(sales_entropy(np.array([2, 1, 1])) - 1.5) <= 1e-15
     assert sales_entropy(np.zeros(5)) == 0.0
+
+
+# ------------------------------------------------------------ step sizes and residual pins
+def _dense_A(inst):
+    """The SBLP capacity matrix written out densely: row j (product), one
+    column per variable y_ij, coefficient 1 where segment i considers j
+    (P:L229-239 Eq. 8; SURVEY D11: A = [M | I])."""
+    A = np.zeros((inst.N, inst.nnz))
+    A[inst.prod_idx, np.arange(inst.nnz)] = 1.0
+    return A
+
+
+def test_tau_is_the_inverse_squared_row_norm_of_A():
+    """c8 (Pock-Chambolle diagonal preconditioning): tau_j = tau0 / ||A_j||^2
+    with A the dense capacity matrix (||A_j||^2 = n_j, P:L1111-1125's rho
+    corrected, SURVEY 0.4 #3); tau_mode 0 is the scalar tau (P:L344)."""
+    inst = generate("small", m=120, N=60, k=(5, 30))
+    A = _dense_A(inst)
+    row2 = (A * A).sum(axis=1)
+    tau1 = oracle.OracleSolver(inst, tau=0.9, tau_mode=1).tau_j
+    want = np.where(row2 > 0, 0.9 / np.maximum(row2, 1.0), 0.9)
+    assert np.array_equal(tau1, want)
+    tau0 = oracle.OracleSolver(inst, tau=0.1, tau_mode=0).tau_j
+    assert np.all(tau0 == 0.1)
+
+
+def test_bundle_tau_is_the_row_sum_of_Bt_A():
+    """c17: per resource tau_l = tau0 / sum_col |(Bt A)_l,col|, Bt the dense
+    bundle -> resource incidence (P:L719-741 Eq. 33)."""
+    from spfom_inputs import with_bundles
+    inst = with_bundles(generate("small", m=120, N=60, k=(5, 30)), L=25, seed=3)
+    Bt = np.zeros((inst.num_resources, inst.N))
+    for j in range(inst.N):
+        Bt[inst.bundle_res[inst.bundle_ptr[j]:inst.bundle_ptr[j + 1]], j] = 1.0
+    rows = np.abs(Bt @ _dense_A(inst)).sum(axis=1)
+    tau = oracle.OracleSolver(inst, tau=0.9, tau_mode=1).tau_j
+    assert np.allclose(tau, np.where(rows > 0, 0.9 / np.maximum(rows, 1.0), 0.9), rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("seed", [1, 11])
+def test_complementary_slackness_vanishes_at_the_lp_optimum(seed):
+    """c11 compl_slack = sum_j eta_j |c_j - s_j| / (1 + |P|): at a primal-dual
+    optimal pair of the LP every positive dual has a binding capacity (KKT
+    complementary slackness), so the converged iterate gives ~0, while an
+    arbitrary positive eta with slack capacities gives a positive value."""
+    inst = generate("tiny", seed=seed)
+    S = oracle.OracleSolver(inst)
+    S.run(2000)
+    res = S.residuals()
+    assert res["compl_slack"] <= 1e-9 and res["rel_gap"] <= 1e-9
+    s = _dense_A(inst) @ S.y
+    eta = np.ones(inst.N)
+    slack = S.residuals(eta=eta)["compl_slack"]
+    assert slack == pytest.approx(np.abs(inst.capacity - s).sum() / (1 + abs(res["primal_obj"])), rel=1e-12)
+    assert slack > 0.0
+
+
+def test_l2_infeasibility_is_bracketed_by_the_max_infeasibility():
+    """c11 infeas_rel_l2 = ||(s - c)^+||_2 / (1 + ||c||_2) against infeas_abs =
+    ||(s - c)^+||_inf: inf-norm <= 2-norm <= sqrt(N) inf-norm; both 0 exactly
+    when every capacity holds."""
+    inst = generate("small", m=200, N=80, k=(5, 30))
+    S = oracle.OracleSolver(inst)
+    S.run(3)                               # early: capacities violated
+    r = S.residuals()
+    cn = np.linalg.norm(inst.capacity[inst.present])
+    lo, hi = r["infeas_abs"] / (1 + cn), np.sqrt(inst.N) * r["infeas_abs"] / (1 + cn)
+    assert r["infeas_abs"] > 0 and lo * (1 - 1e-12) <= r["infeas_rel_l2"] <= hi * (1 + 1e-12)
+    y0 = np.asarray(inst.arrival, float).copy()
+    r0 = S.residuals(eta=np.zeros(inst.N), y=np.zeros(inst.nnz), y0=y0)    # y = 0: s = 0 <= c
+    assert r0["infeas_abs"] == 0.0 and r0["infeas_rel_l2"] == 0.0
