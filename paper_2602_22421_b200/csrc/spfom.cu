@@ -69,18 +69,16 @@ NcclApi &nccl() {
 thread_local std::string g_create_error;
 
 // Bin = (G lanes per segment, Q quads per lane) -> capacity 4 G Q entries.
-// (G lanes per segment, Q quads per lane); capacities 16 .. 1024 entries.
-#ifndef SPFOM_BIN2_G
-#define SPFOM_BIN2_G 4   // 8 segments per warp: the per-warp Newton / reduction overhead is shared by more rows
-#define SPFOM_BIN2_Q 4
-#endif
-// E > 0: rows of at most E quads; the full-sweep stream kernel uses the entry
-// mapping (4 lanes x E entries, StreamLayout), the other kernels the (G, Q) one.
+// E > 0: the full-sweep stream kernel maps E entries per lane on G lanes
+// (rows of up to E G entries, StreamLayout); the other kernels use (G, Q).
 #ifndef SPFOM_BIN_E
-#define SPFOM_BIN_E 13   // k = 49..52 entries (the BASELINE k = 50 configs)
+#define SPFOM_BIN_E 13   // G = 4: k = 49..52 entries exactly fill the lanes (the BASELINE k = 50 configs)
 #endif
-#define SPFOM_BINS(X) X(0, 4, 1, 0) X(1, 4, 2, 0) X(2, 4, 4, SPFOM_BIN_E) X(3, SPFOM_BIN2_G, SPFOM_BIN2_Q, 0) \
-    X(4, 16, 2, 0) X(5, 32, 2, 0) X(6, 32, 4, 0) X(7, 32, 8, 0)
+// Bins 2-4 are entry-mapped in the full-sweep stream kernel: E entries per lane
+// on G = 4 / 8 / 16 lanes, rows of up to 52 / 104 / 208 entries (StreamLayout);
+// every other kernel treats a bin as the quad mapping (G, Q).
+#define SPFOM_BINS(X) X(0, 4, 1, 0) X(1, 4, 2, 0) X(2, 4, 4, SPFOM_BIN_E) X(3, 8, 4, SPFOM_BIN_E) \
+    X(4, 16, 4, SPFOM_BIN_E) X(5, 32, 4, 0) X(6, 32, 8, 0)
 struct BinCfg { int G, Q, E; };
 #define SPFOM_BIN_INIT(B, G, Q, E) {G, Q, E},
 constexpr BinCfg kBins[] = {SPFOM_BINS(SPFOM_BIN_INIT)};
@@ -93,7 +91,7 @@ constexpr int wide_q(int G, int Q) { return G * Q / wide_g(G, Q); }
 
 constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
 
-constexpr int64_t bin_cap(const BinCfg &c) { return c.E > 0 ? c.E : (int64_t)c.G * c.Q; }   // quads
+constexpr int64_t bin_cap(const BinCfg &c) { return c.E > 0 ? (int64_t)c.E * c.G / 4 : (int64_t)c.G * c.Q; }   // quads
 
 int bin_of(int64_t nq) {
     for (int b = 0; b < kNumBins; ++b)
@@ -395,8 +393,9 @@ void mp_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int
 #define CASE(B, G, Q, E)                                                                   \
     case B:                                                                                \
         if constexpr (Q <= 4) {                                                            \
-            if (argmax) launch_mp<G, Q, true, E>(S, L, sms, st);                           \
-            else launch_mp<G, Q, false, E>(S, L, sms, st);                                 \
+            constexpr int EM = G == 4 ? E : 0;   /* shared periods: entry mapping on 4 lanes only */ \
+            if (argmax) launch_mp<G, Q, true, EM>(S, L, sms, st);                          \
+            else launch_mp<G, Q, false, EM>(S, L, sms, st);                                \
         }                                                                                  \
         break;
         SPFOM_BINS(CASE)
@@ -1160,7 +1159,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     h->qoff_h = qoff;
     for (int b = 0; b < kNumBins; ++b) {
         const int64_t k0 = h->bin_first[b], k1 = h->bin_first[b + 1];
-        h->bin_uniform[b] = kBins[b].E > 0 && k1 > k0 && (int64_t)qoff[k1] - qoff[k0] == (k1 - k0) * kBins[b].E;
+        h->bin_uniform[b] = kBins[b].E > 0 && kBins[b].G == 4 && k1 > k0 &&
+                            (int64_t)qoff[k1] - qoff[k0] == (k1 - k0) * kBins[b].E;
     }
     ptimer.mark("padded CSR (omp)");
     // ---- sampled block tables: per (iteration, bin) lists of device slots
@@ -1316,7 +1316,9 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             // B200, medium config: an SM streams ~20 KB/us of a 4-lane bin, 16.0 of a
             // 16-lane and 13.6 of a 32-lane one (wider groups: more butterfly steps and
             // fewer segments per warp round), so wide bins get proportionally more SMs
-            const double cost = kBins[b].G >= 32 ? 1.5 : (kBins[b].G >= 16 ? 1.28 : 1.0);
+            // (entry-mapped bins: 13 entries per lane; wider groups pay deeper butterflies)
+            const double cost = kBins[b].E > 0 ? (kBins[b].G >= 16 ? 1.12 : kBins[b].G >= 8 ? 1.05 : 1.0)
+                                               : (kBins[b].G >= 32 ? 1.5 : (kBins[b].G >= 16 ? 1.28 : 1.0));
             w[b] = pl.sampled ? cnt * bin_cap(kBins[b])
                               : (int64_t)(cost * (double)((int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt));
             if (cnt > 0) h->nbins_active += 1;

@@ -471,18 +471,22 @@ __device__ __forceinline__ void release_work(unsigned long long *work) {
 #ifndef SPFOM_STREAM_WARPS_WIDE
 #define SPFOM_STREAM_WARPS_WIDE 8    // 16 entries per lane
 #endif
-// EQ > 0: entry mapping for rows of at most EQ quads (G = 4): lane l of a
-// group takes entry l of every quad of the row, so a lane holds EQ entries
-// instead of 4 Q -- no lane computes on pad quads when the rows are EQ quads
-// long (huge: k = 50 -> 13 quads, 19% less per-entry work than the (4, 4) bin)
+// EQ > 0: entry mapping, EQ entries per lane for rows of at most EQ G
+// entries (RQ = EQ G / 4 quads): lane l of a G-lane group takes entries l,
+// l + G, l + 2 G, .. of the row (entry e = element e % 4 of quad e / 4).  With
+// G = 4 that is entry l of every quad, and no lane computes on pad quads when
+// the rows are EQ quads long (huge: k = 50 -> 13 quads, 19% less per-entry
+// work than the (4, 4) bin); G = 8 / 16 serve rows of up to 104 / 208 entries
+// with the same 13 entries per lane (medium).
 template <int G, int Q, int EQ = 0>
 struct StreamLayout {
-    static_assert(EQ == 0 || G == 4, "entry mapping: 4 lanes per segment");
+    static_assert(EQ == 0 || G % 4 == 0, "entry mapping: a multiple of 4 lanes per segment");
     static constexpr int NE = EQ ? EQ : 4 * Q;         // entries per lane
+    static constexpr int RQ = EQ ? EQ * G / 4 : G * Q; // quads per row, at most
     // one persistent block per SM; warps per block from the register budget
     static constexpr int WARPS = EQ ? SPFOM_STREAM_WARPS_E : ((4 * Q >= 16) ? SPFOM_STREAM_WARPS_WIDE : SPFOM_STREAM_WARPS);
     static constexpr int GPW = 32 / G;                 // segments per round (per warp)
-    static constexpr int QMAX = GPW * (EQ ? EQ : G * Q);   // quads per round, at most
+    static constexpr int QMAX = GPW * RQ;              // quads per round, at most
     static constexpr int QW = ((GPW + 8) + 3) & ~3;    // qoff window of the next round (ints)
     static constexpr uint32_t OFF_SEGV = 0;                            // double4 x GPW
     static constexpr uint32_t OFF_SEGC = 32u * GPW;                    // double2 x GPW
@@ -507,7 +511,7 @@ struct StreamList {
     int32_t ghead;          // g staged in shared memory for products [0, ghead)
     int32_t hh;             // group histograms cover products [0, hh) (<= Layout::HH)
     unsigned long long *work;   // dynamic round chunks: counter zeroed before the launch
-    int32_t uni;            // entry mapping: every row of the bin has exactly EQ quads
+    int32_t uni;            // entry mapping, G = 4: every row of the bin has exactly EQ quads
 };
 
 template <int G, int Q, int EQ = 0>
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 
     // uniform entry-mapped bin: every row has EQ quads, so a segment's quad
     // offset is arithmetic (no qoff reads, no window copy per round)
-    const bool uni = EQ > 0 && L.uni;
+    const bool uni = EQ > 0 && G == 4 && L.uni;
     const int32_t qbase = uni ? S.qoff[L.first] : 0;
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
@@ -712,16 +716,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             // ids first and the price gather right away (a2), so the L2 reads
             // of the tail prices are in flight while v, omega and y are read
             int pos[NE];
-            if (L.uni && left >= GPW) {
-                // uniform rows, full round: group g's row is quads [EQ g, EQ g + EQ) of
-                // the slot -- constant offsets, no per-entry bounds test
+            if (uni && left >= GPW) {
+                // uniform rows (G = 4), full round: group g's row is quads [EQ g, EQ g + EQ)
+                // of the slot -- constant offsets, no per-entry bounds test
 #pragma unroll
                 for (int t = 0; t < EQ; ++t) pos[t] = 4 * (EQ * gidx + t) + gl;
             } else {
+                // entry gl + G t of the row: quad qa + gl / 4 + (G / 4) t, element gl % 4
 #pragma unroll
                 for (int t = 0; t < EQ; ++t) {
-                    const int32_t q = qa + t;
-                    pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + gl;   // no quad: the inert zero quad
+                    const int32_t q = qa + gl / 4 + (G / 4) * t;
+                    pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + (gl & 3);   // no quad: the inert zero quad
                 }
             }
 #pragma unroll
@@ -768,7 +773,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 #ifdef SPFOM_DEVICE_CHECKS
 #pragma unroll
         for (int e = 0; e < NE; ++e) SPFOM_DCHECK(S, idx[e] >= 0 && idx[e] <= N);
-        SPFOM_DCHECK(S, qb - qa <= (EQ > 0 ? EQ : G * Q) && qa >= base && qb - base <= LY::QMAX);
+        SPFOM_DCHECK(S, qb - qa <= LY::RQ && qa >= base && qb - base <= LY::QMAX);
 #endif
         // a2: price gather (g[N] = 0 for pads; head from shared memory).  The
         // opaque copies keep the two bases in registers (otherwise ptxas
@@ -803,16 +808,16 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 
         // ---- write back (y, segment state), a5 usage scatter
         if constexpr (EQ > 0) {
-            // the group's 4 lanes write each quad's 32-B sector
-            double *yp = S.y + 4 * (int64_t)qa + gl;
+            // each quad's 32-B sector is written by 4 lanes of the group
+            double *yp = S.y + 4 * ((int64_t)qa + gl / 4) + (gl & 3);
             SPFOM_DCHECK(S, !active || (int64_t)qb <= S.nq);
-            if (L.uni && left >= GPW) {
+            if (uni && left >= GPW) {
 #pragma unroll
                 for (int t = 0; t < EQ; ++t) yp[4 * t] = yv[t];
             } else {
 #pragma unroll
                 for (int t = 0; t < EQ; ++t)
-                    if (qa + t < qb) yp[4 * t] = yv[t];
+                    if (qa + gl / 4 + (G / 4) * t < qb) yp[G * t] = yv[t];
             }
         } else
 #pragma unroll

@@ -96,9 +96,9 @@ def _ragged_instance(ks, N=1100, seed=0):
 
 def test_ragged_lengths_cross_every_bin_and_pad():
     """Edge cases: k = 0 (empty consideration set), 1, pad widths 1..3, every
-    bin boundary (16/32/64/128/256/512/1024 entries)."""
-    ks = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257,
-          300, 511, 512, 513, 1000, 1024, 0, 6, 50] * 3
+    bin boundary (16/32/52/104/208/512/1024 entries) and the old ones."""
+    ks = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 51, 52, 53, 63, 64, 65, 103, 104, 105, 127, 128, 129,
+          200, 207, 208, 209, 255, 256, 257, 300, 511, 512, 513, 1000, 1024, 0, 6, 50] * 3
     inst = _ragged_instance(ks)
     worst, gpu, cpu = lockstep(inst, _params(), 60)
     gpu.close()
