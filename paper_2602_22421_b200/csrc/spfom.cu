@@ -343,7 +343,7 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
 
 // Full sweep of a contiguous bin: one persistent 12-warp block per SM; the
 // rest of the opt-in shared memory stages the head of g.
-template <int G, int Q, bool ARGMAX, int EQ = 0>
+template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false>
 void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
     using LY = StreamLayout<G, Q, EQ>;
     static PerDevice cache;
@@ -354,7 +354,7 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
-        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX, EQ, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(fixed + (size_t)hg_cap * 8));
     }
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
@@ -362,7 +362,7 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
     const int64_t rounds = (L.count + LY::GPW - 1) / LY::GPW;
     constexpr int W = LY::WARPS;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
-    k_primal_stream<G, Q, ARGMAX, EQ><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+    k_primal_stream<G, Q, ARGMAX, EQ, UNI><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
 // Multi-period shared structure: units = rounds x T over one persistent block per SM.
@@ -419,6 +419,12 @@ void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L,
             if (prefer_wide<G, Q>(L.count, sms) && (WG != G)) {                            \
                 if (argmax) launch_stream<WG, WQ, true>(S, L, sms, st);                    \
                 else launch_stream<WG, WQ, false>(S, L, sms, st);                          \
+            } else if constexpr (E > 0 && G == 4) {                                        \
+                if (L.uni) {                                                               \
+                    if (argmax) launch_stream<G, Q, true, E, true>(S, L, sms, st);         \
+                    else launch_stream<G, Q, false, E, true>(S, L, sms, st);               \
+                } else if (argmax) launch_stream<G, Q, true, E>(S, L, sms, st);            \
+                else launch_stream<G, Q, false, E>(S, L, sms, st);                         \
             } else if (argmax) launch_stream<G, Q, true, E>(S, L, sms, st);                \
             else launch_stream<G, Q, false, E>(S, L, sms, st);                             \
         }                                                                                  \

@@ -491,13 +491,16 @@ struct StreamLayout {
     static constexpr uint32_t OFF_SEGV = 0;                            // double4 x GPW
     static constexpr uint32_t OFF_SEGC = 32u * GPW;                    // double2 x GPW
     static constexpr uint32_t OFF_QW = OFF_SEGC + 16u * GPW;           // int x QW
-    // quad arrays hold QMAX + 1 quads: index QMAX is an inert zero quad (id N,
-    // v = omega = y = 0) that lanes without a quad read instead of branching
-    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u) & ~63u;    // double4 x (QMAX + 1)
-    static constexpr uint32_t OFF_OM = OFF_V + 32u * (QMAX + 1);           // double4 x (QMAX + 1)
-    static constexpr uint32_t OFF_Y = OFF_OM + 32u * (QMAX + 1);           // double4 x (QMAX + 1)
-    static constexpr uint32_t OFF_IDS = OFF_Y + 32u * (QMAX + 1);          // int4 x (QMAX + 1)
-    static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + 1)) + 127u) & ~127u;
+    // quad arrays hold QMAX + NI quads: quads QMAX .. QMAX + NI - 1 are inert
+    // zero quads (id N, v = omega = y = 0) that lanes without a quad read
+    // instead of branching (NI = EQ for the entry mapping on 4 lanes, so that a
+    // whole row of an inactive group maps onto them with constant offsets)
+    static constexpr int NI = (EQ > 0 && G == 4) ? EQ : 1;
+    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u) & ~63u;    // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_OM = OFF_V + 32u * (QMAX + NI);           // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_Y = OFF_OM + 32u * (QMAX + NI);           // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_IDS = OFF_Y + 32u * (QMAX + NI);          // int4 x (QMAX + NI)
+    static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + NI)) + 127u) & ~127u;
     // one head histogram per group (ids are distinct within a segment: no atomics)
     static constexpr int NHIST = GPW;
     static constexpr int HH = (EQ ? SPFOM_HIST_TOTAL_E : SPFOM_HIST_TOTAL) / NHIST;
@@ -519,7 +522,12 @@ __host__ __device__ constexpr size_t stream_smem_fixed() {
     return (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::PER_WARP + 128;   // + mbarriers
 }
 
-template <int G, int Q, bool ARGMAX, int EQ = 0>
+// UNI (entry mapping on 4 lanes, every row of the bin exactly EQ quads): slot
+// positions are compile-time offsets from one per-lane base (an inactive group
+// of the last round points at the inert quads), so the round has no per-entry
+// bounds tests at all -- a separate instantiation, so that the compiler cannot
+// fold the ragged path's index arithmetic into it.
+template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false>
 __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_primal_stream(DevState S, StreamList L) {
     using LY = StreamLayout<G, Q, EQ>;
     constexpr int NE = LY::NE;
@@ -546,11 +554,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
-    if (lane < 4) {   // this warp's inert zero quad (past the quads the copies write)
-        reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[lane] = 0.0;
-        reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[lane] = 0.0;
-        reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[lane] = 0.0;
-        reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[lane] = N;
+    for (int e = lane; e < 4 * LY::NI; e += 32) {   // this warp's inert zero quads (past the quads the copies write)
+        reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[e] = 0.0;
+        reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[e] = 0.0;
+        reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[e] = 0.0;
+        reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[e] = N;
     }
     if (lane == 0) {
         mbar_init(bar, 1);
@@ -609,7 +617,8 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 
     // uniform entry-mapped bin: every row has EQ quads, so a segment's quad
     // offset is arithmetic (no qoff reads, no window copy per round)
-    const bool uni = EQ > 0 && G == 4 && L.uni;
+    static_assert(!UNI || (EQ > 0 && G == 4), "uniform rows: entry mapping on 4 lanes");
+    constexpr bool uni = UNI;
     const int32_t qbase = uni ? S.qoff[L.first] : 0;
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
@@ -716,11 +725,12 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             // ids first and the price gather right away (a2), so the L2 reads
             // of the tail prices are in flight while v, omega and y are read
             int pos[NE];
-            if (uni && left >= GPW) {
-                // uniform rows (G = 4), full round: group g's row is quads [EQ g, EQ g + EQ)
-                // of the slot -- constant offsets, no per-entry bounds test
+            if constexpr (UNI) {
+                // uniform rows: group g's row is quads [EQ g, EQ g + EQ) of the slot; an
+                // inactive group (last round) reads the EQ inert quads instead
+                const int pb = 4 * (active ? EQ * gidx : LY::QMAX) + gl;
 #pragma unroll
-                for (int t = 0; t < EQ; ++t) pos[t] = 4 * (EQ * gidx + t) + gl;
+                for (int t = 0; t < EQ; ++t) pos[t] = pb + 4 * t;
             } else {
                 // entry gl + G t of the row: quad qa + gl / 4 + (G / 4) t, element gl % 4
 #pragma unroll
@@ -811,9 +821,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             // each quad's 32-B sector is written by 4 lanes of the group
             double *yp = S.y + 4 * ((int64_t)qa + gl / 4) + (gl & 3);
             SPFOM_DCHECK(S, !active || (int64_t)qb <= S.nq);
-            if (uni && left >= GPW) {
+            if constexpr (UNI) {
+                if (active) {
 #pragma unroll
-                for (int t = 0; t < EQ; ++t) yp[4 * t] = yv[t];
+                    for (int t = 0; t < EQ; ++t) yp[4 * t] = yv[t];
+                }
             } else {
 #pragma unroll
                 for (int t = 0; t < EQ; ++t)
