@@ -1979,6 +1979,16 @@ void spfom_destroy(spfom_handle *h) {
 
 }  // extern "C"
 
+#ifdef SPFOM_DIAG_SPAN
+extern "C" int spfom_diag_span(unsigned long long *out, int reset) {
+    int e = (int)cudaMemcpyFromSymbol(out, spfom::g_diag_span, 4 * 160 * sizeof(unsigned long long));
+    if (reset) {
+        static unsigned long long z[4 * 160] = {0};
+        cudaMemcpyToSymbol(spfom::g_diag_span, z, sizeof z);
+    }
+    return e;
+}
+#endif
 #ifdef SPFOM_DIAG_PHASE
 extern "C" int spfom_diag_phase(unsigned long long *out, int reset) {
     int e = (int)cudaMemcpyFromSymbol(out, spfom::g_diag_phase, 10 * sizeof(unsigned long long));

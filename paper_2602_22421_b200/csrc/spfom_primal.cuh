@@ -188,6 +188,15 @@ __device__ __forceinline__ double check_out(double z, double v, double om, doubl
 //   SPFOM_DIAG_RED_FROM=j0  global reductions only for products >= j0
 //   SPFOM_DIAG_SEP_USAGE    no usage scatter in K1; A y recomputed by k_usage before K3
 //                           (+ SPFOM_DIAG_SEP_DUMMY: K1 still scatters, into discarded copies)
+#ifdef SPFOM_DIAG_SPAN
+// diagnostic: per block of the last K1 launch, %globaltimer at entry, after
+// the block setup, the latest warp's loop end, and exit (after the flush)
+__device__ unsigned long long g_diag_span[4 * 160];
+#define SPAN_MARK(k) do { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+    if ((k) == 2) atomicMax(&g_diag_span[4 * blockIdx.x + 2], t_); else if (threadIdx.x == 0) g_diag_span[4 * blockIdx.x + (k)] = t_; } while (0)
+#else
+#define SPAN_MARK(k) do { } while (0)
+#endif
 #ifdef SPFOM_DIAG_PHASE
 // [0] mbarrier wait, [1] slot read + gather + step, [2] projection, [3] y /
 // state write-back, [4] head histograms, [5] global reductions, [6] rounds,
@@ -445,6 +454,23 @@ __device__ __forceinline__ void release_work(unsigned long long *work) {
     }
 }
 
+// Block setup: the head of g (products [0, HG)) into shared memory as one TMA
+// bulk copy on its own mbarrier (thread 0 issues it; every thread waits on
+// gbar after the block's setup barrier).  A strided copy loop was ~7 us of
+// every launch's prologue (exp/span.py).
+__device__ __forceinline__ void ghead_issue(double *ghead, const double *g, int HG, uint64_t *gbar) {
+    if (threadIdx.x == 0 && HG > 0) {
+        mbar_init(gbar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = ((uint32_t)HG * 8u + 15u) & ~15u;   // g holds >= N + 2 slots
+        mbar_arrive_expect_tx(gbar, bytes);
+        bulk_g2s(ghead, g, bytes, gbar);
+    }
+}
+__device__ __forceinline__ void ghead_wait(int HG, uint64_t *gbar) {
+    if (HG > 0) mbar_wait(gbar, 0);
+}
+
 // ============================================================== k_primal_stream
 // Full sweep over segments [first, first + count) of one bin (contiguous).
 #ifndef SPFOM_SPREAD_C
@@ -529,6 +555,7 @@ __host__ __device__ constexpr size_t stream_smem_fixed() {
 // fold the ragged path's index arithmetic into it.
 template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false>
 __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_primal_stream(DevState S, StreamList L) {
+    SPAN_MARK(0);
     using LY = StreamLayout<G, Q, EQ>;
     constexpr int NE = LY::NE;
     constexpr int GPW = LY::GPW;
@@ -665,12 +692,15 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     }
     // block setup while the first round is in flight: the head of g and
     // zeroed group histograms
-    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
+    uint64_t *gbar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + LY::WARPS;
+    ghead_issue(ghead, S.g, HG, gbar);
     for (int w = 0; w < LY::WARPS; ++w) {
         double *h = reinterpret_cast<double *>(smem + (size_t)w * LY::PER_WARP + LY::SLOT);
         for (int j = threadIdx.x; j < LY::NHIST * HS; j += blockDim.x) h[j] = 0.0;
     }
     __syncthreads();
+    ghead_wait(HG, gbar);
+    SPAN_MARK(1);
 #ifdef SPFOM_DIAG_TIME
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
@@ -884,6 +914,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     if (lane == 0)
         for (int k = 0; k < 10; ++k) atomicAdd(&g_diag_phase[k], (unsigned long long)ph[k]);
 #endif
+    if (lane == 0) SPAN_MARK(2);
 #ifdef SPFOM_DIAG_TIME
     if (lane == 0) {
         g_diag_loops[4 * (blockIdx.x * LY::WARPS + warp)] = (uint32_t)(wait_cycles >> 10);
@@ -917,6 +948,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             if (sum != 0.0) atomicAdd(S.s + j, sum);
         }
     }
+    SPAN_MARK(3);
 }
 
 // ============================================================== k_primal_mp
@@ -987,7 +1019,8 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
 
-    for (int j = threadIdx.x; j < HG; j += blockDim.x) ghead[j] = S.g[j];
+    uint64_t *gbar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + 2 * LY::WARPS;
+    ghead_issue(ghead, S.g, HG, gbar);
     if (lane < 4) {   // inert zero quads
         reinterpret_cast<double *>(ws + LY::S_V + 32u * LY::QMAX)[lane] = 0.0;
         reinterpret_cast<double *>(ws + LY::S_OM + 32u * LY::QMAX)[lane] = 0.0;
@@ -1000,6 +1033,7 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
         fence_mbar_init();
     }
     __syncthreads();
+    ghead_wait(HG, gbar);
 
     // Whole rounds (all T periods of GPW base segments) per claim: warps take
     // rounds from a global counter (SPFOM_DYN_CH_MP > 0; see k_primal_stream)
