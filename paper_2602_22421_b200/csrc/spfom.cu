@@ -498,6 +498,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 SL.count = cnt;
                 SL.work = slot_ptr<unsigned long long>(h, O_WORK) + 2 * b;   // reset by the launch's last block
                 SL.uni = h->bin_uniform[b] ? 1 : 0;
+                SL.qbase = h->qoff_h[h->bin_first[b]];
                 // several bins: concurrent persistent kernels on disjoint SM shares
                 // (forked streams; inside a graph they become parallel branches)
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;

@@ -541,6 +541,7 @@ struct StreamList {
     int32_t hh;             // group histograms cover products [0, hh) (<= Layout::HH)
     unsigned long long *work;   // dynamic round chunks: counter zeroed before the launch
     int32_t uni;            // entry mapping, G = 4: every row of the bin has exactly EQ quads
+    int32_t qbase;          // qoff[first] (host copy: no load on the launch's critical path)
 };
 
 template <int G, int Q, int EQ = 0>
@@ -646,7 +647,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     // offset is arithmetic (no qoff reads, no window copy per round)
     static_assert(!UNI || (EQ > 0 && G == 4), "uniform rows: entry mapping on 4 lanes");
     constexpr bool uni = UNI;
-    const int32_t qbase = uni ? S.qoff[L.first] : 0;
+    const int32_t qbase = uni ? L.qbase : 0;
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
         int64_t k = GPW * r + (lane < GPW ? lane : GPW);
