@@ -89,6 +89,9 @@ constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
 constexpr int wide_g(int G, int Q) { return G * Q <= 32 ? G * Q : 32; }
 constexpr int wide_q(int G, int Q) { return G * Q / wide_g(G, Q); }
 
+#ifndef SPFOM_SAMPLED_STREAM
+#define SPFOM_SAMPLED_STREAM 1   // sampled blocks through the stream kernels (0: list kernels)
+#endif
 constexpr int64_t kMaxQuads = 4 * 32 * 8 / 4 * 1;  // 256 quads = 1024 entries
 
 constexpr int64_t bin_cap(const BinCfg &c) { return c.E > 0 ? (int64_t)c.E * c.G / 4 : (int64_t)c.G * c.Q; }   // quads
@@ -343,18 +346,18 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
 
 // Full sweep of a contiguous bin: one persistent 12-warp block per SM; the
 // rest of the opt-in shared memory stages the head of g.
-template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false>
+template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false, bool SAMP = false>
 void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
     using LY = StreamLayout<G, Q, EQ>;
     static PerDevice cache;
     int &hg_cap = *cache.slot();
-    constexpr size_t fixed = stream_smem_fixed<G, Q, EQ>();
+    constexpr size_t fixed = stream_smem_fixed<G, Q, EQ, SAMP>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         hg_cap = (int)std::min<int64_t>(kGHeadStreamMax, std::max<int64_t>(0, ((int64_t)optin - (int64_t)fixed) / 8 / 32 * 32));
-        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX, EQ, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_primal_stream<G, Q, ARGMAX, EQ, UNI, SAMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(fixed + (size_t)hg_cap * 8));
     }
     L.ghead = (int32_t)std::min<int64_t>(hg_cap, S.N + 1);
@@ -362,7 +365,7 @@ void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t s
     const int64_t rounds = (L.count + LY::GPW - 1) / LY::GPW;
     constexpr int W = LY::WARPS;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(sm_count, (rounds + W - 1) / W));
-    k_primal_stream<G, Q, ARGMAX, EQ, UNI><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
+    k_primal_stream<G, Q, ARGMAX, EQ, UNI, SAMP><<<(unsigned)blocks, 32 * W, fixed + (size_t)L.ghead * 8, st>>>(S, L);
 }
 
 // Multi-period shared structure: units = rounds x T over one persistent block per SM.
@@ -410,6 +413,8 @@ bool prefer_wide(int64_t count, int sms) {
     return rounds < 2 * (int64_t)sms * StreamLayout<G, Q>::WARPS;
 }
 
+// SAMP: the same kernels over this iteration's block list (sampled blocks).
+template <bool SAMP = false>
 void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L, int sms, cudaStream_t st) {
     switch (b) {
 #define CASE(B, G, Q, E)                                                                   \
@@ -417,16 +422,16 @@ void stream_dispatch(int b, bool argmax, const DevState &S, const StreamList &L,
         if constexpr (Q <= 4) {                                                            \
             constexpr int WG = wide_g(G, Q), WQ = wide_q(G, Q);                            \
             if (prefer_wide<G, Q>(L.count, sms) && (WG != G)) {                            \
-                if (argmax) launch_stream<WG, WQ, true>(S, L, sms, st);                    \
-                else launch_stream<WG, WQ, false>(S, L, sms, st);                          \
+                if (argmax) launch_stream<WG, WQ, true, 0, false, SAMP>(S, L, sms, st);    \
+                else launch_stream<WG, WQ, false, 0, false, SAMP>(S, L, sms, st);          \
             } else if constexpr (E > 0 && G == 4) {                                        \
                 if (L.uni) {                                                               \
-                    if (argmax) launch_stream<G, Q, true, E, true>(S, L, sms, st);         \
-                    else launch_stream<G, Q, false, E, true>(S, L, sms, st);               \
-                } else if (argmax) launch_stream<G, Q, true, E>(S, L, sms, st);            \
-                else launch_stream<G, Q, false, E>(S, L, sms, st);                         \
-            } else if (argmax) launch_stream<G, Q, true, E>(S, L, sms, st);                \
-            else launch_stream<G, Q, false, E>(S, L, sms, st);                             \
+                    if (argmax) launch_stream<G, Q, true, E, true, SAMP>(S, L, sms, st);   \
+                    else launch_stream<G, Q, false, E, true, SAMP>(S, L, sms, st);         \
+                } else if (argmax) launch_stream<G, Q, true, E, false, SAMP>(S, L, sms, st); \
+                else launch_stream<G, Q, false, E, false, SAMP>(S, L, sms, st);           \
+            } else if (argmax) launch_stream<G, Q, true, E, false, SAMP>(S, L, sms, st);   \
+            else launch_stream<G, Q, false, E, false, SAMP>(S, L, sms, st);                \
         }                                                                                  \
         break;
         SPFOM_BINS(CASE)
@@ -488,6 +493,24 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
             L.row_off = slot_ptr<int32_t>(h, O_ROWOFF);
             L.block_iters = h->params.block_iters;
             maxc = h->pl.bin_count[b] > 0 ? std::min<int64_t>(h->pl.bin_count[b], h->params.block_size) : 0;
+            if (SPFOM_SAMPLED_STREAM && maxc > 0 && kBins[b].Q <= 4 && h->T == 1) {
+                // the block's rows of this bin gathered into the stream kernel's slots
+                StreamList SL{};
+                SL.first = h->bin_first[b];
+                SL.count = maxc;
+                SL.work = slot_ptr<unsigned long long>(h, O_WORK) + 2 * b;
+                SL.uni = h->bin_uniform[b] ? 1 : 0;
+                SL.qbase = h->qoff_h[h->bin_first[b]];
+                SL.ids = L.ids;
+                SL.row_off = L.row_off;
+                SL.bin = b;
+                SL.nbins = kNumBins;
+                SL.block_iters = L.block_iters;
+                const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
+                stream_dispatch<true>(b, argmax, S, SL, sms, h->nbins_active > 1 ? h->side[b] : h->stream);
+                ++nl;
+                continue;
+            }
         } else {
             // full sweep: the bin is the contiguous device range [bin_first[b], bin_first[b+1])
             const int64_t cnt = h->bin_first[b + 1] - h->bin_first[b];

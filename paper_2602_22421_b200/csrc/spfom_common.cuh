@@ -128,6 +128,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // L2 evict-first policy for data streamed once per iteration (keeps g, the
 // usage accumulators and the per-segment state resident in L2)
+// 16-B global -> shared copy through L2 only (.cg: no L1 allocation), and
+// the per-thread group commit / wait (sampled stream kernel's row gather)
+__device__ __forceinline__ void cp16_g2s(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));

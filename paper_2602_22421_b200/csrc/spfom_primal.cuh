@@ -479,6 +479,9 @@ __device__ __forceinline__ void ghead_wait(int HG, uint64_t *gbar) {
 #ifndef SPFOM_HIST_TOTAL
 #define SPFOM_HIST_TOTAL 1024      // head products privatised per warp (split over its groups)
 #endif
+#ifndef SPFOM_SAMP_BULK
+#define SPFOM_SAMP_BULK 0   // sampled rounds: 1 = one bulk copy per (row, array); 0 = 16-B cp.async over the lanes
+#endif
 #ifndef SPFOM_DYN_CH
 #define SPFOM_DYN_CH 2   // rounds per dynamically claimed chunk (0: static contiguous partition per warp)
 #endif
@@ -542,11 +545,20 @@ struct StreamList {
     unsigned long long *work;   // dynamic round chunks: counter zeroed before the launch
     int32_t uni;            // entry mapping, G = 4: every row of the bin has exactly EQ quads
     int32_t qbase;          // qoff[first] (host copy: no load on the launch's critical path)
+    // sampled blocks (SAMP instantiations): this iteration's segments of the
+    // bin are ids[row_off[r][bin] .. row_off[r][bin + 1]), r = t mod block_iters
+    // (device slots of the bin, count = an upper bound for the grid)
+    const int32_t *ids;
+    const int32_t *row_off;
+    int32_t bin, nbins;
+    int64_t block_iters;
 };
 
-template <int G, int Q, int EQ = 0>
+// + mbarriers; SAMP: + each warp's copy of y_old (NE x 32 lanes) for the usage delta
+template <int G, int Q, int EQ = 0, bool SAMP = false>
 __host__ __device__ constexpr size_t stream_smem_fixed() {
-    return (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::PER_WARP + 128;   // + mbarriers
+    return (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::PER_WARP + 128 +
+           (SAMP ? (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::NE * 256 : 0);
 }
 
 // UNI (entry mapping on 4 lanes, every row of the bin exactly EQ quads): slot
@@ -554,7 +566,15 @@ __host__ __device__ constexpr size_t stream_smem_fixed() {
 // of the last round points at the inert quads), so the round has no per-entry
 // bounds tests at all -- a separate instantiation, so that the compiler cannot
 // fold the ragged path's index arithmetic into it.
-template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false>
+//
+// SAMP (sampled blocks, "Randomly generate a subset of customers I"):
+// the rounds are GPW consecutive entries of this iteration's block list of the
+// bin instead of GPW consecutive device slots.  The rows are not contiguous,
+// so the slot is filled by 16-B cp.async copies (each row's quads are
+// contiguous: a few copies per row and array, spread over the lanes) instead
+// of one bulk copy per array; the compute is the same, and the usage scatter
+// adds y_new - y_old (Alg. 2's sum over [n] keeps the rows outside I_t).
+template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false, bool SAMP = false>
 __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_primal_stream(DevState S, StreamList L) {
     SPAN_MARK(0);
     using LY = StreamLayout<G, Q, EQ>;
@@ -576,8 +596,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     unsigned char *slot = smem + (size_t)warp * LY::PER_WARP;
     double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + warp;
-    double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q, EQ>());
+    double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q, EQ, SAMP>());
     double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) + gidx * HS;
+    // SAMP: entry e of this lane's y_old at yo_s + 256 e (conflict-free)
+    const uint32_t yo_s = smem_u32(smem + (size_t)LY::WARPS * LY::PER_WARP + 128) + (uint32_t)warp * (NE * 256u) + 8u * lane;
+    (void)yo_s;
     const uint32_t ghead_s = smem_u32(ghead), hg_s = smem_u32(hg);
     const int spread_n = S.spread_n;
     const int spread_rel = S.spread_off + ((blockIdx.x * LY::WARPS + warp) % (S.spread_c > 0 ? S.spread_c : 1)) * spread_n;
@@ -608,7 +631,16 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     // end); the next chunk is claimed one chunk ahead, so the atomic's latency
     // is hidden.  Rounds come from a 3-deep queue q0 (current), q1 (its TMA
     // is issued during q0), q2 (q1's copy also fetches q2's offsets).
-    const int32_t rounds = (int32_t)((L.count + GPW - 1) / GPW);
+    int64_t count = L.count;
+    const int32_t *sids = nullptr;
+    if constexpr (SAMP) {
+        const int64_t row = (*S.t) % L.block_iters;
+        const int32_t *ro = L.row_off + row * (L.nbins + 1);
+        const int32_t a = ro[L.bin];
+        count = ro[L.bin + 1] - a;
+        sids = L.ids + a;
+    }
+    const int32_t rounds = (int32_t)((count + GPW - 1) / GPW);
     constexpr int CH = SPFOM_DYN_CH;
     const int32_t nch = CH > 0 ? (rounds + CH - 1) / CH : 0;
     // the claimed chunk id stays in lane 0's register until the warp moves to
@@ -651,8 +683,85 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     // lane l <= GPW: qoff of segment GPW r + l of the bin (clamped to the bin end)
     auto qload = [&](int64_t r) -> int32_t {
         int64_t k = GPW * r + (lane < GPW ? lane : GPW);
-        k = k < L.count ? k : L.count;
+        k = k < count ? k : count;
         return uni ? qbase + (int32_t)(EQ * k) : S.qoff[L.first + k];
+    };
+    // SAMP: lane l < GPW: device slot of round r's segment l (-1: none)
+    auto sload = [&](int64_t r) -> int32_t {
+        const int64_t k = GPW * r + lane;
+        return (lane < GPW && k < count) ? __ldg(sids + k) : -1;
+    };
+    // SAMP: quad range [gq, ge) of slot sid (loads only: the first use is in issue_s)
+    auto sdesc = [&](int32_t sid, int32_t &gq, int32_t &ge) {
+        if (sid < 0) {
+            gq = 0;
+            ge = 0;
+        } else if constexpr (UNI) {
+            gq = qbase + EQ * (sid - (int32_t)L.first);
+            ge = gq + EQ;
+        } else {
+            gq = __ldg(S.qoff + sid);
+            ge = __ldg(S.qoff + sid + 1);
+        }
+    };
+    // SAMP: gather round's rows into the slot: row l at local quad lq (the
+    // exclusive prefix of the row lengths; EQ l for uniform rows)
+    auto issue_s = [&](int32_t sid, int32_t gq, int32_t ge, int32_t &lq) {
+        const int32_t nq = ge - gq;
+        if constexpr (UNI) {
+            lq = EQ * lane;
+        } else {
+            int32_t inc = nq;
+#pragma unroll
+            for (int d = 1; d < GPW; d <<= 1) {
+                const int32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += t;
+            }
+            lq = inc - nq;
+        }
+#if SPFOM_SAMP_BULK
+        // one bulk copy per (row, array), issued by the row's lane; lane 0
+        // arms the barrier with the round's bytes first
+        const int32_t totq = __shfl_sync(0xffffffffu, lq + nq, GPW - 1);
+        const uint32_t nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, sid >= 0));
+        if (lane == 0) mbar_arrive_expect_tx(bar, 48u * nrows + 112u * (uint32_t)totq);
+        __syncwarp();
+        if (sid >= 0) {
+            bulk_g2s(slot + LY::OFF_SEGV + 32u * lane, S.segv + sid, 32u, bar);
+            bulk_g2s(slot + LY::OFF_SEGC + 16u * lane, S.segc + sid, 16u, bar);
+            if (nq > 0) {
+                bulk_g2s(slot + LY::OFF_IDS + 16u * lq, S.pidx + gq, 16u * nq, bar);
+                bulk_g2s(slot + LY::OFF_V + 32u * lq, S.v + 4 * (int64_t)gq, 32u * nq, bar);
+                bulk_g2s(slot + LY::OFF_OM + 32u * lq, S.om + 4 * (int64_t)gq, 32u * nq, bar);
+                bulk_g2s(slot + LY::OFF_Y + 32u * lq, S.y + 4 * (int64_t)gq, 32u * nq, bar);
+            }
+        }
+#else
+        const uint32_t sb = smem_u32(slot);
+        if (sid >= 0) {
+            const double *sv = reinterpret_cast<const double *>(S.segv + sid);
+            cp16_g2s(sb + LY::OFF_SEGV + 32u * lane, sv);
+            cp16_g2s(sb + LY::OFF_SEGV + 32u * lane + 16u, sv + 2);
+            cp16_g2s(sb + LY::OFF_SEGC + 16u * lane, S.segc + sid);
+        }
+#pragma unroll 1
+        for (int j = 0; j < GPW; ++j) {
+            const int32_t gj = __shfl_sync(0xffffffffu, gq, j);
+            const int32_t nj = __shfl_sync(0xffffffffu, nq, j);
+            const int32_t lj = __shfl_sync(0xffffffffu, lq, j);
+            if (nj == 0) continue;         // empty row (k = 0) or no row
+            SPFOM_DCHECK(S, nj <= LY::RQ && lj + nj <= LY::QMAX && gj >= 0 && (int64_t)gj + nj <= S.nq);
+            for (int c = lane; c < nj; c += 32) cp16_g2s(sb + LY::OFF_IDS + 16u * (uint32_t)(lj + c), S.pidx + gj + c);
+            for (int c = lane; c < 2 * nj; c += 32) {
+                const int64_t o = 4 * (int64_t)gj + 2 * c;
+                const uint32_t d = 32u * (uint32_t)lj + 16u * (uint32_t)c;
+                cp16_g2s(sb + LY::OFF_V + d, S.v + o);
+                cp16_g2s(sb + LY::OFF_OM + d, S.om + o);
+                cp16_g2s(sb + LY::OFF_Y + d, S.y + o);
+            }
+        }
+        cp_commit();
+#endif
     };
     // lane 0 issues the bulk copies of round r (q: this lane's qoff of round r):
     // segment state, quads, and (rw >= 0) the 16-B aligned qoff window that
@@ -660,7 +769,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     auto issue = [&](int64_t r, int32_t q, int64_t rw) {
         const int32_t qa = __shfl_sync(0xffffffffu, q, 0), qb = __shfl_sync(0xffffffffu, q, GPW);
         const int64_t s0 = L.first + GPW * r;
-        const int64_t left = L.count - GPW * r;
+        const int64_t left = count - GPW * r;
         const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
         const int64_t w0 = (L.first + GPW * rw) & ~(int64_t)3;        // window of round rw
@@ -687,7 +796,17 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     ProjStats st;
     int32_t qc = 0;
     int32_t q0 = fnext(), q1 = fnext(), q2 = fnext();
-    if (q0 >= 0) {
+    // SAMP: per lane (< GPW), round q0: slot ss0, quads [sg0, se0), local sl0;
+    // round q1: ss1, [sg1, se1), sl1; round q2: ss2
+    int32_t ss0 = -1, sg0 = 0, se0 = 0, sl0 = 0, ss1 = -1, sg1 = 0, se1 = 0, sl1 = 0, ss2 = -1;
+    if constexpr (SAMP) {
+        if (q0 >= 0) {
+            ss0 = sload(q0);
+            sdesc(ss0, sg0, se0);
+            issue_s(ss0, sg0, se0, sl0);
+        }
+        if (q1 >= 0) ss1 = sload(q1);
+    } else if (q0 >= 0) {
         qc = qload(q0);
         issue(q0, qc, q1);
     }
@@ -715,28 +834,48 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         PH_MARK(7);
 #ifdef SPFOM_DIAG_TIME
         const long long tw0 = clock64();
-        mbar_wait(bar, phase);
+#endif
+        if constexpr (SAMP && !SPFOM_SAMP_BULK) {
+            cp_wait_all();
+            __syncwarp();
+        } else {
+            mbar_wait(bar, phase);
+        }
+#ifdef SPFOM_DIAG_TIME
         wait_cycles += clock64() - tw0;
         const long long tr0 = clock64();
-#else
-        mbar_wait(bar, phase);
 #endif
         PH_MARK(0);
+        if constexpr (SAMP) {
+            // ids of round q2 and the quad ranges of round q1 (used by issue_s)
+            ss2 = q2 >= 0 ? sload(q2) : -1;
+            sdesc(ss1, sg1, se1);
+        }
         // round q1's offsets from the window that arrived with this round
         int32_t qn = 0;
-        if (q1 >= 0) {
+        if (!SAMP && q1 >= 0) {
             const int64_t s1 = L.first + GPW * (int64_t)q1;
             int64_t k = GPW * (int64_t)q1 + (lane < GPW ? lane : GPW);
-            k = k < L.count ? k : L.count;
+            k = k < count ? k : count;
             qn = uni ? qbase + (int32_t)(EQ * k)
                      : reinterpret_cast<const int32_t *>(slot + LY::OFF_QW)[L.first + k - (s1 & ~(int64_t)3)];
         }
-        const int32_t base = __shfl_sync(0xffffffffu, qc, 0);
-        const int32_t qa = __shfl_sync(0xffffffffu, qc, gidx);
-        const int32_t qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
-        const int64_t left = L.count - GPW * r;
+        int32_t base, qa, qb;
+        int64_t i;
+        if constexpr (SAMP) {
+            // group gidx: row ss0 of lane gidx, global quads [qa, qb), local from qa - base
+            qa = __shfl_sync(0xffffffffu, sg0, gidx);
+            qb = __shfl_sync(0xffffffffu, se0, gidx);
+            base = qa - __shfl_sync(0xffffffffu, sl0, gidx);
+            i = __shfl_sync(0xffffffffu, ss0, gidx);
+        } else {
+            base = __shfl_sync(0xffffffffu, qc, 0);
+            qa = __shfl_sync(0xffffffffu, qc, gidx);
+            qb = __shfl_sync(0xffffffffu, qc, gidx + 1);
+            i = L.first + GPW * r + gidx;
+        }
+        const int64_t left = count - GPW * r;
         const bool active = gidx < left;
-        const int64_t i = L.first + GPW * r + gidx;
 
         // ---- segment state and this lane's quads, from the slot
         double lam = 1.0, vt0 = 1.0;
@@ -801,6 +940,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             om[4 * t + 0] = w01.x; om[4 * t + 1] = w01.y; om[4 * t + 2] = w23.x; om[4 * t + 3] = w23.y;
             z[4 * t + 0] = y01.x; z[4 * t + 1] = y01.y; z[4 * t + 2] = y23.x; z[4 * t + 3] = y23.y;
         }
+        if constexpr (SAMP) {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) sts_f64(yo_s + 256u * e, z[e]);   // y_old (z is y until a3)
+        }
         // the slot is free: fetch round r + 1 into it while this round computes.
         // The warp barrier orders every lane's slot reads before the copy is
         // issued (the consumer-release pattern of TMA pipelines); a
@@ -808,7 +951,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         // wait for the previous round's global reductions to drain.
         PH_MARK(1);
         __syncwarp();
-        if (q1 >= 0) issue(q1, qn, q2);
+        if constexpr (SAMP) {
+            if (q1 >= 0) issue_s(ss1, sg1, se1, sl1);
+        } else if (q1 >= 0) {
+            issue(q1, qn, q2);
+        }
         PH_MARK(8);
 
 #ifdef SPFOM_DEVICE_CHECKS
@@ -869,6 +1016,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             if (q < qb) st256_stream(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
         if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+        if constexpr (SAMP) {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) yv[e] -= lds_f64_v(yo_s + 256u * e);   // a5 delta: y_new - y_old
+        }
         PH_MARK(3);
 #ifdef SPFOM_DIAG_TIME
         const long long ts0 = clock64();
@@ -906,6 +1057,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         (void)tr0;
 #endif
         qc = qn;
+        if constexpr (SAMP) {
+            ss0 = ss1; sg0 = sg1; se0 = se1; sl0 = sl1;
+            ss1 = ss2;
+        }
         PH_MARK(5);
 #ifdef SPFOM_DIAG_PHASE
         ph[6] += 1;

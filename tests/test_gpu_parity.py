@@ -121,6 +121,37 @@ def test_entry_mapped_bin_lockstep(preset, k):
     _assert_ok(worst)
 
 
+@pytest.mark.parametrize("preset", ["paper", "converge"])
+@pytest.mark.parametrize("case", ["uniform E13", "ragged E13", "medium bins", "medium wide", "every bin"])
+def test_sampled_stream_lockstep(case, preset):
+    """Sampled blocks through the stream kernels' row gather (SAMP
+    instantiations, exec_mode 1 = graph): the block's rows of each bin are
+    gathered into the slots by 16-B copies and the usage scatter adds
+    y_new - y_old.  uniform E13: k = 50 (13 quads, the UNI path) with
+    N = 20000 > the shared/spread head, so the tail reductions run; ragged:
+    33..52 entries (per-entry bounds); medium bins: blocks big enough for the
+    throughput mappings of the G = 4 / 8 / 16 entry-mapped bins; medium wide:
+    small blocks (the wide latency mappings).  Per-iterate rel-inf <= 1e-10 vs
+    the oracle run on the same blocks."""
+    if case == "uniform E13":
+        inst, B, it = generate("huge", m=48005, N=20000, k=50), 24001, 60
+    elif case == "ragged E13":
+        inst, B, it = generate("huge", m=48005, N=3000, k=(33, 52)), 24001, 60
+    elif case == "medium bins":
+        inst, B, it = generate("medium", m=100000, N=6000, k=(20, 200)), 60000, 30
+    elif case == "medium wide":
+        inst, B, it = generate("medium", m=8000, N=3000, k=(20, 200)), 1500, 100
+    else:                       # k = 0 rows, pads, every bin boundary (the longest rows: list kernel)
+        ks = [0, 1, 3, 4, 5, 16, 17, 32, 33, 52, 53, 104, 105, 208, 209, 512, 513, 1000] * 40
+        inst, B, it = _ragged_instance(ks, N=1100, seed=5), 400, 60
+    blocks = block_sequence(inst.m, B, 16, seed=9)
+    p = _params(blocks=blocks, exec_mode=1) if preset == "converge" else _paper(mu=0.5, blocks=blocks, exec_mode=1)
+    worst, gpu, _ = lockstep(inst, p, it, blocks=blocks, check_every=5, check_first=3)
+    assert not gpu.info()["persistent"]
+    gpu.close()
+    _assert_ok(worst)
+
+
 def test_mnl_special_case_lockstep():
     """omega = 0 (MNL) is the GAM special case."""
     inst = generate("small", m=500, N=300, k=(10, 80))
