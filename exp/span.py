@@ -1,5 +1,6 @@
 """Prologue / loop / epilogue of one K1 launch per block (-DSPFOM_DIAG_SPAN) on
-rank 0's shard of a P-way partition of huge (PS env, default 1,8)."""
+rank 0's shard of a P-way partition of huge (PS env, default 1,8); FRAC > 1:
+sampled blocks of m / FRAC rows."""
 import ctypes as C, os, sys
 sys.path.insert(0, ".")
 import numpy as np
@@ -12,7 +13,10 @@ buf = np.zeros(4 * 160, dtype=np.uint64)
 for P in [int(x) for x in os.environ.get("PS", "1,8").split(",")]:
     b = partition(inst.seg_ptr, P)
     shard = inst.segment_slice(int(b[0]), int(b[1])) if P > 1 else inst
-    s = Solver(shard, Params.converge(), device="cuda:0")
+    frac = int(os.environ.get("FRAC", "1"))      # > 1: sampled blocks B = m / FRAC of the shard
+    from spfom_inputs import block_sequence
+    blocks = None if frac == 1 else block_sequence(shard.m, shard.m // frac, 16, 11)
+    s = Solver(shard, Params.converge(blocks=blocks, exec_mode=1), device="cuda:0")
     s.step(20)
     res = []
     for rep in range(5):

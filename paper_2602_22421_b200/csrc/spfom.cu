@@ -7,6 +7,7 @@
 // caller's workspace -> initial state (reading c10).
 // step: CUDA-graph replay of one iteration (K1 per bin -> NCCL allreduce of
 // the usage accumulator -> K3 [-> averaging] -> tick).
+#include <cuda.h>            // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <time.h>
@@ -89,6 +90,9 @@ constexpr int kNumBins = sizeof(kBins) / sizeof(kBins[0]);
 constexpr int wide_g(int G, int Q) { return G * Q <= 32 ? G * Q : 32; }
 constexpr int wide_q(int G, int Q) { return G * Q / wide_g(G, Q); }
 
+#ifndef SPFOM_SAMP_G4
+#define SPFOM_SAMP_G4 1   // sampled uniform bins: whole rows by TMA tile::gather4 (0: per-row bulk copies)
+#endif
 #ifndef SPFOM_SAMPLED_STREAM
 #define SPFOM_SAMPLED_STREAM 1   // sampled blocks through the stream kernels (0: list kernels)
 #endif
@@ -154,7 +158,7 @@ struct Plan {
 enum Slot {
     O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
     O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
-    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_WORK, O_NSLOTS
+    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_WORK, O_TMAPS, O_NSLOTS
 };
 
 constexpr int kSpreadCopies = SPFOM_SPREAD_C;
@@ -221,6 +225,7 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_COUNTERS] = 8 * 8;
     sz[O_T] = 8;
     sz[O_WORK] = 16 * kNumBins;  // K1 stream: dynamic round-chunk counter + exited-block count, per bin
+    sz[O_TMAPS] = pl.sampled ? (size_t)kNumBins * 6 * sizeof(CUtensorMap) : 0;   // sampled uniform bins: gather4 maps
     sz[O_COUNTS] = N1 * 8;
     // recovery scratch (spfom_recover works in chunks of at most recover_chunk() padded entries)
     sz[O_RECORD] = (size_t)recover_chunk(pl.nq) * 4;
@@ -253,6 +258,7 @@ struct spfom_handle {
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> qoff_h;               // device-order quad offsets [m + 1] (host copy)
     bool bin_uniform[kNumBins] = {false};      // entry-mapped bin whose rows all have exactly E quads
+    const void *bin_tmaps[kNumBins] = {nullptr};   // sampled uniform bins: 6 gather4 tensor maps (device)
     double *pin[2] = {nullptr, nullptr};       // pinned D2H staging ring (getters), allocated on first use
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     std::vector<int32_t> bin_first;            // [kNumBins+1] first device slot of each bin
@@ -348,10 +354,10 @@ void launch_primal(const DevState &S, SegList L, int64_t max_count, int sm_count
 // rest of the opt-in shared memory stages the head of g.
 template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false, bool SAMP = false>
 void launch_stream(const DevState &S, StreamList L, int sm_count, cudaStream_t st) {
-    using LY = StreamLayout<G, Q, EQ>;
+    using LY = StreamLayout<G, Q, EQ, SAMP && UNI>;
     static PerDevice cache;
     int &hg_cap = *cache.slot();
-    constexpr size_t fixed = stream_smem_fixed<G, Q, EQ, SAMP>();
+    constexpr size_t fixed = stream_smem_fixed<G, Q, EQ, SAMP, UNI>();
     if (hg_cap < 0) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
@@ -472,6 +478,61 @@ void resid_dispatch(int b, const DevState &S, const SegList &L, double *part, in
 
 // Enqueue one iteration (used under stream capture).  refresh: sampled-mode
 // fresh recompute of s = A y before the dual step.
+// Sampled blocks on uniform bins (every row E quads): 2-D tensor maps over the
+// bin's rows for TMA tile::gather4 -- ids / v / omega / y as [rows][4 E]
+// (row pitch 16 E / 32 E bytes), segv [rows][4], segc [rows][2]; box {cols, 1}.
+// Without the driver's encoder (or if it rejects a map) the bin keeps the
+// per-row bulk copies.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+spfom_status encode_gather_maps(spfom_handle *h) {
+    static EncodeTiledFn enc = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = reinterpret_cast<EncodeTiledFn>(fn);
+    });
+    if (!enc) return SPFOM_OK;
+    const DevState &S = h->S;
+    std::vector<CUtensorMap> maps((size_t)kNumBins * 6);
+    bool any = false;
+    for (int b = 0; b < kNumBins; ++b) {
+        const int64_t rows = h->bin_first[b + 1] - h->bin_first[b];
+        if (!h->bin_uniform[b] || rows == 0 || kBins[b].E == 0) continue;
+        const int E = kBins[b].E;
+        const int64_t first = h->bin_first[b], q0 = h->qoff_h[first];
+        struct A { CUtensorMapDataType dt; void *base; cuuint64_t cols, pitch; };
+        const A arr[6] = {{CU_TENSOR_MAP_DATA_TYPE_INT32, (void *)(S.pidx + q0), (cuuint64_t)4 * E, (cuuint64_t)16 * E},
+                          {CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (void *)(S.v + 4 * q0), (cuuint64_t)4 * E, (cuuint64_t)32 * E},
+                          {CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (void *)(S.om + 4 * q0), (cuuint64_t)4 * E, (cuuint64_t)32 * E},
+                          {CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (void *)(S.y + 4 * q0), (cuuint64_t)4 * E, (cuuint64_t)32 * E},
+                          {CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (void *)(S.segv + first), 4, 32},
+                          {CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (void *)(S.segc + first), 2, 16}};
+        bool ok = true;
+        for (int a = 0; a < 6 && ok; ++a) {
+            const cuuint64_t dims[2] = {arr[a].cols, (cuuint64_t)rows};
+            const cuuint64_t strides[1] = {arr[a].pitch};
+            const cuuint32_t box[2] = {(cuuint32_t)arr[a].cols, 1}, es[2] = {1, 1};
+            ok = enc(&maps[(size_t)b * 6 + a], arr[a].dt, 2, arr[a].base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        if (!ok) continue;
+        h->bin_tmaps[b] = slot_ptr<unsigned char>(h, O_TMAPS) + (size_t)b * 6 * sizeof(CUtensorMap);
+        any = true;
+    }
+    if (any) {
+        CUDA_TRY(h, cudaMemcpyAsync(slot_ptr<unsigned char>(h, O_TMAPS), maps.data(), maps.size() * sizeof(CUtensorMap),
+                                    cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    }
+    return SPFOM_OK;
+}
+
 // a1-a5: the primal kernels, one launch per non-empty length bin
 spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
     const bool argmax = std::isinf(h->params.theta);
@@ -506,6 +567,7 @@ spfom_status enqueue_primal(spfom_handle *h, int64_t *launches) {
                 SL.bin = b;
                 SL.nbins = kNumBins;
                 SL.block_iters = L.block_iters;
+                SL.tm = h->bin_tmaps[b];
                 const int sms = h->nbins_active > 1 ? h->bin_sms[b] : h->sm_count;
                 stream_dispatch<true>(b, argmax, S, SL, sms, h->nbins_active > 1 ? h->side[b] : h->stream);
                 ++nl;
@@ -1302,6 +1364,11 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.max_newton = h->params.max_newton;
     S.sampled = pl.sampled ? 1 : 0;
 
+    // sampled uniform bins: TMA tensor maps for tile::gather4 of whole rows
+    if (pl.sampled && T == 1 && SPFOM_SAMP_G4) {
+        st = encode_gather_maps(h);
+        if (st != SPFOM_OK) return bail(st);
+    }
     // small regime (exec_mode 0 auto / 2 forced): whole iterations per cooperative launch
     {
         int64_t max_rq = 0;

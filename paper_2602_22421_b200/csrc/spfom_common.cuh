@@ -128,6 +128,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // L2 evict-first policy for data streamed once per iteration (keeps g, the
 // usage accumulators and the per-segment state resident in L2)
+// TMA tile::gather4 (sm_100a): 4 rows of a 2-D tensor (box {cols, 1}) with
+// arbitrary row coordinates, landing as 4 packed rows at dst
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void *tmap, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3, uint64_t *bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;"
+                 ::"r"(dst), "l"(tmap), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(pol)
+                 : "memory");
+}
 // 16-B global -> shared copy through L2 only (.cg: no L1 allocation), and
 // the per-thread group commit / wait (sampled stream kernel's row gather)
 __device__ __forceinline__ void cp16_g2s(uint32_t dst, const void *src) {

@@ -480,7 +480,7 @@ __device__ __forceinline__ void ghead_wait(int HG, uint64_t *gbar) {
 #define SPFOM_HIST_TOTAL 1024      // head products privatised per warp (split over its groups)
 #endif
 #ifndef SPFOM_SAMP_BULK
-#define SPFOM_SAMP_BULK 0   // sampled rounds: 1 = one bulk copy per (row, array); 0 = 16-B cp.async over the lanes
+#define SPFOM_SAMP_BULK 1   // sampled rounds: 1 = one bulk copy per (row, array); 0 = 16-B cp.async over the lanes
 #endif
 #ifndef SPFOM_DYN_CH
 #define SPFOM_DYN_CH 2   // rounds per dynamically claimed chunk (0: static contiguous partition per warp)
@@ -507,7 +507,11 @@ __device__ __forceinline__ void ghead_wait(int HG, uint64_t *gbar) {
 // the rows are EQ quads long (huge: k = 50 -> 13 quads, 19% less per-entry
 // work than the (4, 4) bin); G = 8 / 16 serve rows of up to 104 / 208 entries
 // with the same 13 entries per lane (medium).
-template <int G, int Q, int EQ = 0>
+// TA (sampled uniform rows, TMA gather4 into the slot): every gather4
+// destination 128-B aligned -- the quad arrays start on 128 B, segc rows 4..7
+// and ids rows 4..7 sit 64 B further (the compute adds the shift), and the
+// inert ids move past them.
+template <int G, int Q, int EQ = 0, bool TA = false>
 struct StreamLayout {
     static_assert(EQ == 0 || G % 4 == 0, "entry mapping: a multiple of 4 lanes per segment");
     static constexpr int NE = EQ ? EQ : 4 * Q;         // entries per lane
@@ -519,17 +523,19 @@ struct StreamLayout {
     static constexpr int QW = ((GPW + 8) + 3) & ~3;    // qoff window of the next round (ints)
     static constexpr uint32_t OFF_SEGV = 0;                            // double4 x GPW
     static constexpr uint32_t OFF_SEGC = 32u * GPW;                    // double2 x GPW
-    static constexpr uint32_t OFF_QW = OFF_SEGC + 16u * GPW;           // int x QW
+    static constexpr uint32_t SHIFT = TA ? 64u : 0u;                   // segc / ids rows 4..7 (TA)
+    static constexpr uint32_t OFF_QW = OFF_SEGC + 16u * GPW + SHIFT;   // int x QW
     // quad arrays hold QMAX + NI quads: quads QMAX .. QMAX + NI - 1 are inert
     // zero quads (id N, v = omega = y = 0) that lanes without a quad read
     // instead of branching (NI = EQ for the entry mapping on 4 lanes, so that a
     // whole row of an inactive group maps onto them with constant offsets)
     static constexpr int NI = (EQ > 0 && G == 4) ? EQ : 1;
-    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u) & ~63u;    // double4 x (QMAX + NI)
-    static constexpr uint32_t OFF_OM = OFF_V + 32u * (QMAX + NI);           // double4 x (QMAX + NI)
-    static constexpr uint32_t OFF_Y = OFF_OM + 32u * (QMAX + NI);           // double4 x (QMAX + NI)
-    static constexpr uint32_t OFF_IDS = OFF_Y + 32u * (QMAX + NI);          // int4 x (QMAX + NI)
-    static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + NI)) + 127u) & ~127u;
+    static constexpr uint32_t AL = TA ? 127u : 0u;
+    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u + AL) & ~(63u + AL);   // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_OM = (OFF_V + 32u * (QMAX + NI) + AL) & ~AL;          // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_Y = (OFF_OM + 32u * (QMAX + NI) + AL) & ~AL;          // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_IDS = (OFF_Y + 32u * (QMAX + NI) + AL) & ~AL;         // int4 x (QMAX + NI) (+ SHIFT)
+    static constexpr uint32_t SLOT = ((OFF_IDS + 16u * (QMAX + NI) + SHIFT) + 127u) & ~127u;
     // one head histogram per group (ids are distinct within a segment: no atomics)
     static constexpr int NHIST = GPW;
     static constexpr int HH = (EQ ? SPFOM_HIST_TOTAL_E : SPFOM_HIST_TOTAL) / NHIST;
@@ -552,13 +558,17 @@ struct StreamList {
     const int32_t *row_off;
     int32_t bin, nbins;
     int64_t block_iters;
+    // uniform bins: 6 TMA tensor maps (128 B each, global memory) over the
+    // bin's rows -- ids, v, omega, y as [rows][4 EQ], segv [rows][4], segc
+    // [rows][2] -- for tile::gather4 (null: per-row copies)
+    const void *tm;
 };
 
 // + mbarriers; SAMP: + each warp's copy of y_old (NE x 32 lanes) for the usage delta
-template <int G, int Q, int EQ = 0, bool SAMP = false>
+template <int G, int Q, int EQ = 0, bool SAMP = false, bool UNI = false>
 __host__ __device__ constexpr size_t stream_smem_fixed() {
-    return (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::PER_WARP + 128 +
-           (SAMP ? (size_t)StreamLayout<G, Q, EQ>::WARPS * StreamLayout<G, Q, EQ>::NE * 256 : 0);
+    using LY = StreamLayout<G, Q, EQ, SAMP && UNI>;
+    return (size_t)LY::WARPS * LY::PER_WARP + 128 + (SAMP ? (size_t)LY::WARPS * LY::NE * 256 : 0);
 }
 
 // UNI (entry mapping on 4 lanes, every row of the bin exactly EQ quads): slot
@@ -577,7 +587,7 @@ __host__ __device__ constexpr size_t stream_smem_fixed() {
 template <int G, int Q, bool ARGMAX, int EQ = 0, bool UNI = false, bool SAMP = false>
 __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_primal_stream(DevState S, StreamList L) {
     SPAN_MARK(0);
-    using LY = StreamLayout<G, Q, EQ>;
+    using LY = StreamLayout<G, Q, EQ, SAMP && UNI>;
     constexpr int NE = LY::NE;
     constexpr int GPW = LY::GPW;
     static_assert(NE <= 32, "class bitmasks hold at most 32 entries per lane");
@@ -596,7 +606,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     unsigned char *slot = smem + (size_t)warp * LY::PER_WARP;
     double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)LY::WARPS * LY::PER_WARP) + warp;
-    double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q, EQ, SAMP>());
+    double *ghead = reinterpret_cast<double *>(smem + stream_smem_fixed<G, Q, EQ, SAMP, UNI>());
     double *hg = reinterpret_cast<double *>(smem + (size_t)warp * LY::PER_WARP + LY::SLOT) + gidx * HS;
     // SAMP: entry e of this lane's y_old at yo_s + 256 e (conflict-free)
     const uint32_t yo_s = smem_u32(smem + (size_t)LY::WARPS * LY::PER_WARP + 128) + (uint32_t)warp * (NE * 256u) + 8u * lane;
@@ -609,7 +619,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         reinterpret_cast<double *>(slot + LY::OFF_V + 32u * LY::QMAX)[e] = 0.0;
         reinterpret_cast<double *>(slot + LY::OFF_OM + 32u * LY::QMAX)[e] = 0.0;
         reinterpret_cast<double *>(slot + LY::OFF_Y + 32u * LY::QMAX)[e] = 0.0;
-        reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX)[e] = N;
+        reinterpret_cast<int *>(slot + LY::OFF_IDS + 16u * LY::QMAX + LY::SHIFT)[e] = N;
     }
     if (lane == 0) {
         mbar_init(bar, 1);
@@ -707,6 +717,40 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     // SAMP: gather round's rows into the slot: row l at local quad lq (the
     // exclusive prefix of the row lengths; EQ l for uniform rows)
     auto issue_s = [&](int32_t sid, int32_t gq, int32_t ge, int32_t &lq) {
+        if constexpr (UNI) {
+            if (L.tm != nullptr) {
+                // uniform rows: 4 rows per TMA gather4 per array (rows past the
+                // round's last are copies of its first: the compute masks them)
+                lq = EQ * lane;
+                const int32_t rl = sid - (int32_t)L.first;
+                const int nrows = __popc(__ballot_sync(0xffffffffu, sid >= 0));
+                int32_t rr[GPW];
+#pragma unroll
+                for (int j = 0; j < GPW; ++j) rr[j] = __shfl_sync(0xffffffffu, rl, j < nrows ? j : 0);
+                if (lane == 0) {
+                    constexpr uint32_t ROWB = 16u * EQ + 3u * 32u * EQ + 48u;   // ids, v, om, y, segv, segc
+                    const int ng = (nrows + 3) >> 2;
+                    mbar_arrive_expect_tx(bar, (uint32_t)ng * 4u * ROWB);
+                    const uint64_t pol = l2_evict_first_policy();
+                    const unsigned char *tm = reinterpret_cast<const unsigned char *>(L.tm);
+                    const uint32_t sb = smem_u32(slot);
+#pragma unroll
+                    for (int g4 = 0; g4 < GPW / 4; ++g4) {
+                        if (g4 < ng) {
+                            const int32_t a = rr[4 * g4], b = rr[4 * g4 + 1], c = rr[4 * g4 + 2], d = rr[4 * g4 + 3];
+                            const uint32_t r0 = 4u * g4;
+                            tma_gather4(sb + LY::OFF_IDS + 16u * EQ * r0 + (g4 ? LY::SHIFT : 0u), tm + 0 * 128, a, b, c, d, bar, pol);
+                            tma_gather4(sb + LY::OFF_V + 32u * EQ * r0, tm + 1 * 128, a, b, c, d, bar, pol);
+                            tma_gather4(sb + LY::OFF_OM + 32u * EQ * r0, tm + 2 * 128, a, b, c, d, bar, pol);
+                            tma_gather4(sb + LY::OFF_Y + 32u * EQ * r0, tm + 3 * 128, a, b, c, d, bar, pol);
+                            tma_gather4(sb + LY::OFF_SEGV + 32u * r0, tm + 4 * 128, a, b, c, d, bar, pol);
+                            tma_gather4(sb + LY::OFF_SEGC + 16u * r0 + (g4 ? LY::SHIFT : 0u), tm + 5 * 128, a, b, c, d, bar, pol);
+                        }
+                    }
+                }
+                return;
+            }
+        }
         const int32_t nq = ge - gq;
         if constexpr (UNI) {
             lq = EQ * lane;
@@ -727,13 +771,15 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         if (lane == 0) mbar_arrive_expect_tx(bar, 48u * nrows + 112u * (uint32_t)totq);
         __syncwarp();
         if (sid >= 0) {
+            const uint32_t rsh = lane >= 4 ? LY::SHIFT : 0u;     // TA layout: rows 4..7 of segc / ids
             bulk_g2s(slot + LY::OFF_SEGV + 32u * lane, S.segv + sid, 32u, bar);
-            bulk_g2s(slot + LY::OFF_SEGC + 16u * lane, S.segc + sid, 16u, bar);
+            bulk_g2s(slot + LY::OFF_SEGC + 16u * lane + rsh, S.segc + sid, 16u, bar);
             if (nq > 0) {
-                bulk_g2s(slot + LY::OFF_IDS + 16u * lq, S.pidx + gq, 16u * nq, bar);
-                bulk_g2s(slot + LY::OFF_V + 32u * lq, S.v + 4 * (int64_t)gq, 32u * nq, bar);
-                bulk_g2s(slot + LY::OFF_OM + 32u * lq, S.om + 4 * (int64_t)gq, 32u * nq, bar);
-                bulk_g2s(slot + LY::OFF_Y + 32u * lq, S.y + 4 * (int64_t)gq, 32u * nq, bar);
+                const uint64_t pol = l2_evict_first_policy();
+                bulk_g2s_hint(slot + LY::OFF_IDS + 16u * lq + rsh, S.pidx + gq, 16u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_V + 32u * lq, S.v + 4 * (int64_t)gq, 32u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_OM + 32u * lq, S.om + 4 * (int64_t)gq, 32u * nq, bar, pol);
+                bulk_g2s_hint(slot + LY::OFF_Y + 32u * lq, S.y + 4 * (int64_t)gq, 32u * nq, bar, pol);
             }
         }
 #else
@@ -742,7 +788,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             const double *sv = reinterpret_cast<const double *>(S.segv + sid);
             cp16_g2s(sb + LY::OFF_SEGV + 32u * lane, sv);
             cp16_g2s(sb + LY::OFF_SEGV + 32u * lane + 16u, sv + 2);
-            cp16_g2s(sb + LY::OFF_SEGC + 16u * lane, S.segc + sid);
+            cp16_g2s(sb + LY::OFF_SEGC + 16u * lane + (lane >= 4 ? LY::SHIFT : 0u), S.segc + sid);
         }
 #pragma unroll 1
         for (int j = 0; j < GPW; ++j) {
@@ -751,7 +797,8 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             const int32_t lj = __shfl_sync(0xffffffffu, lq, j);
             if (nj == 0) continue;         // empty row (k = 0) or no row
             SPFOM_DCHECK(S, nj <= LY::RQ && lj + nj <= LY::QMAX && gj >= 0 && (int64_t)gj + nj <= S.nq);
-            for (int c = lane; c < nj; c += 32) cp16_g2s(sb + LY::OFF_IDS + 16u * (uint32_t)(lj + c), S.pidx + gj + c);
+            for (int c = lane; c < nj; c += 32)
+                cp16_g2s(sb + LY::OFF_IDS + 16u * (uint32_t)(lj + c) + (j >= 4 ? LY::SHIFT : 0u), S.pidx + gj + c);
             for (int c = lane; c < 2 * nj; c += 32) {
                 const int64_t o = 4 * (int64_t)gj + 2 * c;
                 const uint32_t d = 32u * (uint32_t)lj + 16u * (uint32_t)c;
@@ -835,7 +882,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
 #ifdef SPFOM_DIAG_TIME
         const long long tw0 = clock64();
 #endif
-        if constexpr (SAMP && !SPFOM_SAMP_BULK) {
+        if (SAMP && !SPFOM_SAMP_BULK && !(UNI && L.tm != nullptr)) {
             cp_wait_all();
             __syncwarp();
         } else {
@@ -882,7 +929,7 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
         if (active) {
             sv = reinterpret_cast<const double4 *>(slot + LY::OFF_SEGV)[gidx];
-            const double2 sc = reinterpret_cast<const double2 *>(slot + LY::OFF_SEGC)[gidx];
+            const double2 sc = *reinterpret_cast<const double2 *>(slot + LY::OFF_SEGC + 16u * gidx + (gidx >= 4 ? LY::SHIFT : 0u));
             lam = sc.x;
             vt0 = sc.y;
         }
@@ -909,8 +956,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
                     pos[t] = 4 * (q < qb ? q - base : LY::QMAX) + (gl & 3);   // no quad: the inert zero quad
                 }
             }
+            // TA layout: ids of rows 4..7 and the inert ids sit SHIFT bytes further
+            const int ish = (LY::SHIFT != 0 && (gidx >= 4 || !active)) ? (int)(LY::SHIFT / 4) : 0;
 #pragma unroll
-            for (int t = 0; t < EQ; ++t) idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[pos[t]];
+            for (int t = 0; t < EQ; ++t) idx[t] = reinterpret_cast<const int *>(slot + LY::OFF_IDS)[pos[t] + ish];
             uint32_t gh_s = ghead_s;
             const double *gglob = S.g;
             asm volatile("" : "+r"(gh_s), "+l"(gglob));
