@@ -86,15 +86,18 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel="k_primal"):
+def ncu_traffic(workload: str, kernel="k_primal"):
     """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu --set full summary (profiles/ncu_summary.json), or None."""
+    ncu --set full summary (profiles/ncu_summary.json) of THIS workload, or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        e = d.get(kernel, {})
+        if e.get("workload", "huge") != workload:
+            return None
+        return e.get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -441,7 +444,7 @@ def main():
     k1_bytes = 20 * shard.nnz // T + 16 * shard.nnz + 4 * shard.m // T + 32 * shard.m
     k1_achieved = k1_bytes / (k1_ms / 1e3) / 1e9
     iter_bytes = (20 * inst.nnz // T + 16 * inst.nnz + 4 * inst.m // T + 32 * inst.m) + BYTES_PER_PRODUCT * inst.N
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.config)
 
     # e2e through the public API with host buffers: create (H2D) + K steps + duals/primal (D2H)
     barrier()

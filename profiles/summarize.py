@@ -184,7 +184,8 @@ def main():
     summ_path = os.path.join(HERE, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     summ["k_primal"] = {"round": rnd, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                        "duration": m["gpu__time_duration.sum"], "source": os.path.basename(rep)}
+                        "duration": m["gpu__time_duration.sum"], "source": os.path.basename(rep),
+                        "workload": os.environ.get("WORKLOAD", "huge")}
     json.dump(summ, open(summ_path, "w"), indent=1)
     if launches:
         shutil.copy(launches, os.path.join(HERE, f"{rnd}_launches.csv"))
