@@ -148,6 +148,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Plan {
     int64_t m = 0, N = 0, nq = 0, T = 1;   // m, nq: base segments / quads; T periods (shared structure)
     int64_t bin_count[kNumBins] = {0};
+    double bin_work[kNumBins] = {0};   // sampled: mean over block rows of the bin's padded quads + rows
     int64_t block_entries = 0;      // total local sampled ids
     bool sampled = false;
     bool averaging = false;
@@ -1266,7 +1267,10 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             const int32_t *row = p->blocks + t * p->block_size;
             for (int64_t b = 0; b < p->block_size; ++b) {
                 const int64_t li = (int64_t)row[b] - off;
-                if (li >= 0 && li < m) per[segbin[li]].push_back(snew[li]);
+                if (li >= 0 && li < m) {
+                    per[segbin[li]].push_back(snew[li]);
+                    h->pl.bin_work[segbin[li]] += (double)(qoff[snew[li] + 1] - qoff[snew[li]] + 1) / (double)p->block_iters;
+                }
             }
             int32_t *ro = rowoff.data() + t * (kNumBins + 1);
             ro[0] = (int32_t)blkids.size();
@@ -1404,8 +1408,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         }
     }
     // several active bins: concurrent launches on SM shares proportional to each bin's work
-    // (full sweep: padded entries x the bin's measured cost per entry; sampled: the largest
-    // per-iteration count x capacity)
+    // (padded entries x the bin's measured cost per entry; sampled: the mean over the
+    // block rows of the bin's padded entries)
     if (!h->small) {
         int64_t wtot = 0, w[kNumBins] = {0};
         for (int b = 0; b < kNumBins; ++b) {
@@ -1416,7 +1420,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             // (entry-mapped bins: 13 entries per lane; wider groups pay deeper butterflies)
             const double cost = kBins[b].E > 0 ? (kBins[b].G >= 16 ? 1.12 : kBins[b].G >= 8 ? 1.05 : 1.0)
                                                : (kBins[b].G >= 32 ? 1.5 : (kBins[b].G >= 16 ? 1.28 : 1.0));
-            w[b] = pl.sampled ? cnt * bin_cap(kBins[b])
+            w[b] = pl.sampled ? (int64_t)(cost * h->pl.bin_work[b])
                               : (int64_t)(cost * (double)((int64_t)qoff[h->bin_first[b + 1]] - (int64_t)qoff[h->bin_first[b]] + cnt));
             if (cnt > 0) h->nbins_active += 1;
             wtot += w[b];
