@@ -31,7 +31,9 @@ def lockstep(inst, params, iters: int, blocks=None, check_every: int = 1, tie_ma
 
     gpu = gpu if gpu is not None else Solver(inst, params)
     cpu = oracle.OracleSolver(inst, **oracle_kwargs(params))
-    ys, lams, rs = 1.0, float(inst.arrival.max()), float(inst.price.max())
+    ys = 1.0
+    lams = float(inst.arrival.max()) if inst.arrival.size else 1.0     # m = 0: nothing to scale
+    rs = float(inst.price.max())
     worst = dict(y=0.0, y0=0.0, eta=0.0, s=0.0)
     for t in range(iters):
         gpu.step(1)

@@ -105,6 +105,42 @@ def test_ragged_lengths_cross_every_bin_and_pad():
     _assert_ok(worst)
 
 
+def _degenerate_instance(m, N, ks, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = [np.sort(rng.choice(N, k, replace=False)) for k in ks]
+    seg_ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    prod = np.concatenate(rows).astype(np.int32) if sum(ks) else np.zeros(0, np.int32)
+    nnz = prod.shape[0]
+    v = rng.uniform(0.1, 1.0, nnz)
+    w = v * rng.uniform(0.0, 0.5, nnz)
+    cnt = np.bincount(prod, minlength=N)
+    return Instance("degenerate", seg_ptr, prod, v, w, rng.uniform(0.5, 2.0, m), rng.uniform(1.0, 10.0, m),
+                    rng.lognormal(3.0, 0.5, N), np.where(cnt > 0, 0.3, 1.0), cnt > 0, {})
+
+
+@pytest.mark.parametrize("exec_mode", [0, 1])
+@pytest.mark.parametrize("case", ["no segments", "every row empty", "one segment, one product", "B = 1"])
+def test_degenerate_instances(case, exec_mode):
+    """The method's degenerate cases through every execution mode: m = 0 (no
+    primal work: the dual step alone, eta stays 0 on the absent products'
+    slack capacity); rows with k = 0 only (y_i0 = lambda_i, A y = 0); a
+    single segment offered a single product (the k = 1 closed form of the
+    projection); sampled blocks of one segment."""
+    blocks = None
+    if case == "no segments":
+        inst = _degenerate_instance(0, 3, [])
+    elif case == "every row empty":
+        inst = _degenerate_instance(5, 4, [0] * 5)
+    elif case == "one segment, one product":
+        inst = _degenerate_instance(1, 1, [1])
+    else:
+        inst = _degenerate_instance(7, 6, [3, 0, 6, 1, 2, 5, 4])
+        blocks = block_sequence(inst.m, 1, 16, 5)
+    worst, gpu, _ = lockstep(inst, _params(exec_mode=exec_mode, blocks=blocks), 40, blocks=blocks)
+    gpu.close()
+    _assert_ok(worst)
+
+
 @pytest.mark.parametrize("preset,k", [("converge", (49, 52)), ("paper", (49, 52)), ("converge", (33, 52)),
                                       ("converge", 50)])
 def test_entry_mapped_bin_lockstep(preset, k):
