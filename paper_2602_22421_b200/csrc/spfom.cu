@@ -159,7 +159,7 @@ struct Plan {
 enum Slot {
     O_PIDX, O_V, O_OM, O_Y, O_YBAR, O_QOFF, O_SEGC, O_SEGV, O_Y0BAR, O_R, O_C, O_TAU, O_ETA, O_G,
     O_ACC, O_SCUR, O_ETABAR, O_TMP, O_BLKIDS, O_ROWOFF, O_RESSEG, O_RESPROD, O_COUNTERS, O_T,
-    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_WORK, O_TMAPS, O_NSLOTS
+    O_COUNTS, O_RECORD, O_RECALPHA, O_ORIG, O_BPTR, O_BRES, O_RPTR, O_RBUN, O_STILDE, O_RESRES, O_WORK, O_TMAPS, O_SEGD, O_NSLOTS
 };
 
 constexpr int kSpreadCopies = SPFOM_SPREAD_C;
@@ -205,6 +205,7 @@ void make_plan(const spfom_instance *in, const spfom_params *p, Plan &pl) {
     sz[O_QOFF] = (m + 1 + 64) * 4;           // + slack: K1's 16-B qoff windows may read past the end
     sz[O_SEGC] = T * m * 16;                  // [T][m]
     sz[O_SEGV] = T * m * 32;
+    sz[O_SEGD] = T * m * 16;                  // float4 [T][m]
     sz[O_Y0BAR] = pl.averaging ? T * m * 8 : 0;
     const int64_t L = std::max<int64_t>(0, in->num_resources);
     const int64_t D1 = std::max<int64_t>(N1, L + 1);       // duals: products or resources
@@ -1355,7 +1356,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     if (pl.averaging) ok = ok && H2D(O_Y0BAR, y0.data(), T * m * 8);
     auto Z = [&](int slot, size_t bytes) { return bytes == 0 || cudaMemsetAsync(h->ws + h->pl.off[slot], 0, bytes, h->stream) == cudaSuccess; };
     ok = ok && Z(O_Y, T * nq * 32) && Z(O_ETA, std::max<int64_t>(D1, prod_slots(N)) * 8) && Z(O_ACC, (spread_off(N) + (size_t)kSpreadCopies * spread_range(N)) * 8) && Z(O_SCUR, prod_slots(N) * 8) &&
-         Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 16 * kNumBins);
+         Z(O_COUNTERS, 64) && Z(O_T, 8) && Z(O_WORK, 16 * kNumBins) && Z(O_SEGD, T * m * 16);
     if (pl.averaging) ok = ok && Z(O_YBAR, T * nq * 32) && Z(O_ETABAR, D1 * 8);
     if (!ok) { h->err = "H2D copy into workspace failed"; return bail(SPFOM_ECUDA); }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) { h->err = "stream sync after create"; return bail(SPFOM_ECUDA); }
@@ -1369,6 +1370,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     S.qoff = slot_ptr<int32_t>(h, O_QOFF);
     S.segc = slot_ptr<double2>(h, O_SEGC);
     S.segv = slot_ptr<double4>(h, O_SEGV);
+    S.segd = slot_ptr<float4>(h, O_SEGD);
     S.y0bar = pl.averaging ? slot_ptr<double>(h, O_Y0BAR) : nullptr;
     S.r = slot_ptr<double>(h, O_R);
     S.c = slot_ptr<double>(h, O_C);
@@ -1787,6 +1789,8 @@ spfom_status spfom_set_state(spfom_handle *h, const double *y, const double *y0,
     if (!h) return SPFOM_EINVAL;
     DeviceGuard dg_(h->device);
     const int64_t T = h->T;
+    if ((y || y0) && h->m)   // a new iterate: no history to extrapolate the warm starts along
+        CUDA_TRY(h, cudaMemsetAsync(h->S.segd, 0, (size_t)T * h->m * 16, h->stream));
     if (y) {
         std::vector<double> tmp(4 * std::max<int64_t>(T * h->nq, 1), 0.0);
         for (int64_t t = 0; t < T; ++t)

@@ -36,6 +36,8 @@ struct DevState {
     const int32_t *qoff;  // [m+1] quad offsets
     const double2 *segc;  // [m]   (lambda, vt0 = v0 + sum w), read-only
     double4 *segv;        // [m]   (y0, nu, kappa, U): no-purchase iterate + warm start of the projection
+    float4 *segd;         // [m]   last change of (nu, kappa, U) (full-sweep stream kernel: the warm
+                          //       start is extrapolated along it; 0 elsewhere / after set_state)
     double *y0bar;        // [m]   or null
     // per product, N + 1 slots (slot N = dummy of the pads: g = 0)
     const double *r, *c, *tau;

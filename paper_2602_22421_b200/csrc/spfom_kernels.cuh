@@ -254,6 +254,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small(DevState S, SmallArg
             double yv[NE];
             double y0new;
             double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+            constexpr bool EX = SPFOM_EXTRAP && !SAMPLED && !ARGMAX;   // extrapolated warm start (spfom_primal.cuh)
+            float4 sd = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (EX && t + 1 >= SPFOM_EXTRAP_FROM && t + 1 < SPFOM_EXTRAP_UNTIL) {
+                sd = S.segd[i];
+                x0 += (double)sd.x;
+                x1 += (double)sd.y;
+                x2 = fmax(x2 + (double)sd.z, 0.5 * x2);
+            }
             if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, sc.x, sc.y, true, yv, y0new);
             else project_group<G, NE>(z, v, om, sv.x, sc.x, sc.y, true, 0xffffffffu, S.max_newton, x0, x1, x2, yv,
                                       y0new, st);
@@ -262,7 +270,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small(DevState S, SmallArg
                 const int32_t q = q0 + lane + G * tq;
                 if (q < q1) st256(S.y + 4 * (int64_t)q, yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
             }
-            if (lane == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+            if (lane == 0) {
+                st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+                if (EX && t + 1 < SPFOM_EXTRAP_UNTIL)
+                    S.segd[i] = make_float4((float)(x0 - sv.y), (float)(x1 - sv.z), (float)(x2 - sv.w), 0.f);
+            }
 #pragma unroll
             for (int e = 0; e < NE; ++e) {                    // a5
                 const int j = idx[e];

@@ -318,7 +318,10 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
                 const double r1 = fma(-x2, ps.cvv, ps.rva);
                 const double R[3] = {r1 - vt0 * x1, y0c + swy - vt0 * x2, y0c + sy - lam};
                 const double nr = dmax_sel(fabs(R[0]), dmax_sel(fabs(R[1]), fabs(R[2])));   // NaN -> caught below
-                bool done = !(nr > tol);
+                // within tol at the warm start (an extrapolated warm start can be that
+                // close): still one Newton step, so that the output is the exact
+                // solution on its piece (balance / scale residuals at rounding level)
+                bool done = !(nr > tol) && !first;
                 if (!isfinite(nr)) { done = true; failed = true; }
                 if (!done) {
                     if (first || nr <= (1.0 - 1e-4 * step) * Ra) {
@@ -329,7 +332,7 @@ __device__ __forceinline__ void project_group(const double (&z)[NE], const doubl
                         double d[3];
                         if (!newton_dir(J, R, d)) {
                             done = true;
-                            failed = true;
+                            failed = !(nr <= tol);
                         } else {
                             a0 = x0; a1 = x1; a2 = x2;
                             d0 = d[0]; d1 = d[1]; d2 = d[2];
@@ -485,6 +488,22 @@ __device__ __forceinline__ void ghead_wait(int HG, uint64_t *gbar) {
 #ifndef SPFOM_DYN_CH
 #define SPFOM_DYN_CH 2   // rounds per dynamically claimed chunk (0: static contiguous partition per warp)
 #endif
+#ifndef SPFOM_EXTRAP
+// full-sweep stream kernels: the projection's warm start is the segment's last
+// multipliers (nu, kappa, U) plus their last change (linear extrapolation),
+// from iteration SPFOM_EXTRAP_FROM on.  Newton passes in iterations 6-25 of
+// huge (exp/warm_sim.py, a host replica of project_group on the GPU's
+// iterates): 2.28 -> 2.01 per segment, 3.42 -> 2.07 per warp round (the max
+// over its 8 segments, which is what a warp pays).  The projection is exact
+// from any start: only the pass count changes.
+#define SPFOM_EXTRAP 1
+#endif
+#ifndef SPFOM_EXTRAP_FROM
+#define SPFOM_EXTRAP_FROM 5
+#endif
+#ifndef SPFOM_EXTRAP_UNTIL
+#define SPFOM_EXTRAP_UNTIL 1000000000LL   // iterations >= UNTIL: no extrapolation, no history kept
+#endif
 #ifndef SPFOM_DYN_CH_MP
 #define SPFOM_DYN_CH_MP 1   // multi-period kernel: rounds (x T periods) per dynamically claimed chunk
 #endif
@@ -525,13 +544,14 @@ struct StreamLayout {
     static constexpr uint32_t OFF_SEGC = 32u * GPW;                    // double2 x GPW
     static constexpr uint32_t SHIFT = TA ? 64u : 0u;                   // segc / ids rows 4..7 (TA)
     static constexpr uint32_t OFF_QW = OFF_SEGC + 16u * GPW + SHIFT;   // int x QW
+    static constexpr uint32_t OFF_SEGD = OFF_QW + 4u * QW;              // float4 x GPW (full sweep)
     // quad arrays hold QMAX + NI quads: quads QMAX .. QMAX + NI - 1 are inert
     // zero quads (id N, v = omega = y = 0) that lanes without a quad read
     // instead of branching (NI = EQ for the entry mapping on 4 lanes, so that a
     // whole row of an inactive group maps onto them with constant offsets)
     static constexpr int NI = (EQ > 0 && G == 4) ? EQ : 1;
     static constexpr uint32_t AL = TA ? 127u : 0u;
-    static constexpr uint32_t OFF_V = ((OFF_QW + 4u * QW) + 63u + AL) & ~(63u + AL);   // double4 x (QMAX + NI)
+    static constexpr uint32_t OFF_V = ((OFF_SEGD + 16u * GPW) + 63u + AL) & ~(63u + AL);   // double4 x (QMAX + NI)
     static constexpr uint32_t OFF_OM = (OFF_V + 32u * (QMAX + NI) + AL) & ~AL;          // double4 x (QMAX + NI)
     static constexpr uint32_t OFF_Y = (OFF_OM + 32u * (QMAX + NI) + AL) & ~AL;          // double4 x (QMAX + NI)
     static constexpr uint32_t OFF_IDS = (OFF_Y + 32u * (QMAX + NI) + AL) & ~AL;         // int4 x (QMAX + NI) (+ SHIFT)
@@ -602,6 +622,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
     const int N = (int)S.N;
     const int HG = L.ghead, HH = L.hh;
     constexpr int HS = hist_stride(LY::HH);
+    // warm-start extrapolation (full sweep, projection): this iteration is *S.t + 1
+    constexpr bool EX = SPFOM_EXTRAP && !SAMP && !ARGMAX;
+    const int64_t it_ = *S.t + 1;
+    const bool ex_on = EX && it_ >= SPFOM_EXTRAP_FROM && it_ < SPFOM_EXTRAP_UNTIL;   // extrapolate (segd read)
+    const bool ex_rec = EX && it_ < SPFOM_EXTRAP_UNTIL;                              // keep the history (segd written)
 
     unsigned char *slot = smem + (size_t)warp * LY::PER_WARP;
     double *hist_all = reinterpret_cast<double *>(smem + LY::SLOT);   // warp w's hists at w * PER_WARP
@@ -825,9 +850,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         const uint32_t wbytes = (rw >= 0 && !uni) ? 4u * LY::QW : 0u;
         // one elected lane, straight-line: the copies take uniform operands
         if (lane == 0) {
-            mbar_arrive_expect_tx(bar, 48u * n + 112u * nq + wbytes);
+            mbar_arrive_expect_tx(bar, (ex_on ? 64u : 48u) * n + 112u * nq + wbytes);
             bulk_g2s(slot + LY::OFF_SEGV, S.segv + s0, 32u * n, bar);
             bulk_g2s(slot + LY::OFF_SEGC, S.segc + s0, 16u * n, bar);
+            if (ex_on) bulk_g2s(slot + LY::OFF_SEGD, S.segd + s0, 16u * n, bar);
             if (wbytes) bulk_g2s(slot + LY::OFF_QW, S.qoff + w0, wbytes, bar);
             if (nq > 0) {
                 const uint64_t pol = l2_evict_first_policy();
@@ -927,8 +953,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         // ---- segment state and this lane's quads, from the slot
         double lam = 1.0, vt0 = 1.0;
         double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
+        float4 sd = make_float4(0.f, 0.f, 0.f, 0.f);
         if (active) {
             sv = reinterpret_cast<const double4 *>(slot + LY::OFF_SEGV)[gidx];
+            if (ex_on) sd = reinterpret_cast<const float4 *>(slot + LY::OFF_SEGD)[gidx];
             const double2 sc = *reinterpret_cast<const double2 *>(slot + LY::OFF_SEGC + 16u * gidx + (gidx >= 4 ? LY::SHIFT : 0u));
             lam = sc.x;
             vt0 = sc.y;
@@ -1031,6 +1059,11 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
         double yv[NE];
         double y0new;
         double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+        if (EX && ex_on) {
+            x0 += (double)sd.x;
+            x1 += (double)sd.y;
+            x2 = fmax(x2 + (double)sd.z, 0.5 * x2);
+        }
         PH_MARK(1);
 #ifdef SPFOM_DIAG_SKIP_PROJECT
 #pragma unroll
@@ -1064,7 +1097,10 @@ __global__ void __launch_bounds__(32 * StreamLayout<G, Q, EQ>::WARPS, 1) k_prima
             const int32_t q = qa + gl + G * t;
             if (q < qb) st256_stream(S.y + 4 * (int64_t)q, yv[4 * t], yv[4 * t + 1], yv[4 * t + 2], yv[4 * t + 3]);
         }
-        if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+        if (active && gl == 0) {
+            st256(reinterpret_cast<double *>(S.segv + i), y0new, x0, x1, x2);
+            if (ex_rec) S.segd[i] = make_float4((float)(x0 - sv.y), (float)(x1 - sv.z), (float)(x2 - sv.w), 0.f);
+        }
         if constexpr (SAMP) {
 #pragma unroll
             for (int e = 0; e < NE; ++e) yv[e] -= lds_f64_v(yo_s + 256u * e);   // a5 delta: y_new - y_old
@@ -1185,7 +1221,8 @@ struct MPLayout {
     // period slot
     static constexpr uint32_t P_SEGV = S_END;                              // double4 x GPW
     static constexpr uint32_t P_SEGC = P_SEGV + 32u * GPW;                 // double2 x GPW
-    static constexpr uint32_t P_Y = ((P_SEGC + 16u * GPW) + 63u) & ~63u;   // double4 x (QMAX + 1)
+    static constexpr uint32_t P_SEGD = P_SEGC + 16u * GPW;                 // float4 x GPW (warm-start change)
+    static constexpr uint32_t P_Y = ((P_SEGD + 16u * GPW) + 63u) & ~63u;   // double4 x (QMAX + 1)
     static constexpr uint32_t P_END = ((P_Y + 32u * (QMAX + 1)) + 127u) & ~127u;
     // per-lane theta g and usage accumulators, [NE][32 lanes] doubles
     static constexpr uint32_t GT = P_END;
@@ -1200,6 +1237,14 @@ __host__ __device__ constexpr size_t mp_smem_fixed() {
 
 template <int G, int Q, bool ARGMAX, int EQ = 0>
 __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp(DevState S, StreamList L) {
+    // warm-start extrapolation (SPFOM_EXTRAP): this iteration is *S.t + 1
+#ifndef SPFOM_EXTRAP_MP
+#define SPFOM_EXTRAP_MP 1
+#endif
+    constexpr bool EX = SPFOM_EXTRAP && SPFOM_EXTRAP_MP && !ARGMAX;
+    const int64_t it_ = *S.t + 1;
+    const bool ex_on = EX && it_ >= SPFOM_EXTRAP_FROM && it_ < SPFOM_EXTRAP_UNTIL;   // extrapolate (segd read)
+    const bool ex_rec = EX && it_ < SPFOM_EXTRAP_UNTIL;                              // keep the history (segd written)
     using LY = MPLayout<G, Q, EQ>;
     constexpr int NE = LY::NE;
     constexpr int GPW = LY::GPW;
@@ -1305,9 +1350,10 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
         const uint32_t n = (uint32_t)(left < GPW ? left : GPW);
         const uint32_t nq = (uint32_t)(qb - qa);
         if (lane == 0) {
-            mbar_arrive_expect_tx(barP, 48u * n + 32u * nq);
+            mbar_arrive_expect_tx(barP, (ex_on ? 64u : 48u) * n + 32u * nq);
             bulk_g2s(ws + LY::P_SEGV, S.segv + t * mb + s0, 32u * n, barP);
             bulk_g2s(ws + LY::P_SEGC, S.segc + t * mb + s0, 16u * n, barP);
+            if (ex_on) bulk_g2s(ws + LY::P_SEGD, S.segd + t * mb + s0, 16u * n, barP);
             if (nq > 0) bulk_g2s(ws + LY::P_Y, S.y + 4 * (t * nqb + qa), 32u * nq, barP);
         }
     };
@@ -1379,8 +1425,10 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
             phP ^= 1u;
             double lam = 1.0, vt0 = 1.0;
             double4 sv = make_double4(1.0, 0.0, 0.0, 1.0);
+            float4 sd = make_float4(0.f, 0.f, 0.f, 0.f);
             if (active) {
                 sv = reinterpret_cast<const double4 *>(ws + LY::P_SEGV)[gidx];
+                if (ex_on) sd = reinterpret_cast<const float4 *>(ws + LY::P_SEGD)[gidx];
                 const double2 sc = reinterpret_cast<const double2 *>(ws + LY::P_SEGC)[gidx];
                 lam = sc.x;
                 vt0 = sc.y;
@@ -1409,6 +1457,11 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
             double yv[NE];
             double y0new;
             double x0 = sv.y, x1 = sv.z, x2 = sv.w;
+            if (EX && ex_on) {      // warm start extrapolated along the last change (SPFOM_EXTRAP)
+                x0 += (double)sd.x;
+                x1 += (double)sd.y;
+                x2 = fmax(x2 + (double)sd.z, 0.5 * x2);
+            }
             if constexpr (ARGMAX) argmax_group<G, NE>(z, v, om, lam, vt0, active, yv, y0new);
             else project_group<G, NE>(z, v, om, sv.x, lam, vt0, active, gmask, S.max_newton, x0, x1, x2, yv, y0new, st);
 
@@ -1424,7 +1477,10 @@ __global__ void __launch_bounds__(32 * MPLayout<G, Q, EQ>::WARPS, 1) k_primal_mp
                 if (q < qb)
                     st256(S.y + 4 * (t * nqb + q), yv[4 * tq], yv[4 * tq + 1], yv[4 * tq + 2], yv[4 * tq + 3]);
             }
-            if (active && gl == 0) st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
+            if (active && gl == 0) {
+                st256(reinterpret_cast<double *>(S.segv + t * mb + i), y0new, x0, x1, x2);
+                if (ex_rec) S.segd[t * mb + i] = make_float4((float)(x0 - sv.y), (float)(x1 - sv.z), (float)(x2 - sv.w), 0.f);
+            }
             {
                 double hv[NE];                                 // loads first: no serial RMW chain
 #pragma unroll
