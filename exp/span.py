@@ -9,7 +9,7 @@ import bench
 from paper_2602_22421_b200 import Params, Solver, load_library, partition
 inst = bench.load_instance("huge", "/tmp/spfom_cache")
 L = load_library()
-buf = np.zeros(4 * 160, dtype=np.uint64)
+buf = np.zeros(4 * 160 + 80, dtype=np.uint64)   # + the per-SM bin keys (uint32)
 for P in [int(x) for x in os.environ.get("PS", "1,8").split(",")]:
     b = partition(inst.seg_ptr, P)
     shard = inst.segment_slice(int(b[0]), int(b[1])) if P > 1 else inst
@@ -25,7 +25,7 @@ for P in [int(x) for x in os.environ.get("PS", "1,8").split(",")]:
         k1, _ = s.step_timed(1)
         torch.cuda.synchronize()
         L.spfom_diag_span(buf.ctypes.data_as(C.c_void_p), C.c_int(0))
-        sp = buf.reshape(-1, 4)[:148].astype(np.int64)
+        sp = buf[:640].reshape(-1, 4)[:148].astype(np.int64)
         t0 = sp[:, 0].min()
         sp = (sp - t0) / 1e3
         res.append((k1 * 1e3, np.median(sp[:, 0]), sp[:, 0].max(), np.median(sp[:, 1] - sp[:, 0]), np.median(sp[:, 2]), sp[:, 2].max(), np.median(sp[:, 3] - sp[:, 2]), sp[:, 3].max()))

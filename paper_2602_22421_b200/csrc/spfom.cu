@@ -2124,6 +2124,7 @@ void spfom_destroy(spfom_handle *h) {
 #ifdef SPFOM_DIAG_SPAN
 extern "C" int spfom_diag_span(unsigned long long *out, int reset) {
     int e = (int)cudaMemcpyFromSymbol(out, spfom::g_diag_span, 4 * 160 * sizeof(unsigned long long));
+    if (!e) e = (int)cudaMemcpyFromSymbol(out + 4 * 160, spfom::g_diag_key, 160 * sizeof(unsigned int));
     if (reset) {
         static unsigned long long z[4 * 160] = {0};
         cudaMemcpyToSymbol(spfom::g_diag_span, z, sizeof z);

@@ -191,9 +191,14 @@ __device__ __forceinline__ double check_out(double z, double v, double om, doubl
 #ifdef SPFOM_DIAG_SPAN
 // diagnostic: per block of the last K1 launch, %globaltimer at entry, after
 // the block setup, the latest warp's loop end, and exit (after the flush)
+// (indexed by %smid -- one persistent block per SM -- so that concurrent bin
+// launches do not collide; g_diag_key[sm] = the bin's G * 10000 + Q * 100 + EQ)
 __device__ unsigned long long g_diag_span[4 * 160];
-#define SPAN_MARK(k) do { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
-    if ((k) == 2) atomicMax(&g_diag_span[4 * blockIdx.x + 2], t_); else if (threadIdx.x == 0) g_diag_span[4 * blockIdx.x + (k)] = t_; } while (0)
+__device__ unsigned int g_diag_key[160];
+#define SPAN_MARK(k) do { unsigned long long t_; unsigned s_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s_)); \
+    if ((k) == 2) atomicMax(&g_diag_span[4 * s_ + 2], t_); else if (threadIdx.x == 0) { g_diag_span[4 * s_ + (k)] = t_; \
+    if ((k) == 0) g_diag_key[s_] = G * 10000 + Q * 100 + EQ; } } while (0)
 #else
 #define SPAN_MARK(k) do { } while (0)
 #endif
