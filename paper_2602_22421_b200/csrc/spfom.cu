@@ -69,6 +69,41 @@ NcclApi &nccl() {
 
 thread_local std::string g_create_error;
 
+// Large host arrays of create (pos_map, the per-segment state): uninitialised
+// (every element is written by the layout loop; no serial zero-fill), freed
+// with free().  (2 MiB-aligned transparent-huge-page advice was measured on the
+// GPU hosts: no change in create or the getters, so none is given.)
+struct FreeDel { void operator()(void *p) const { free(p); } };
+template <class T>
+static std::unique_ptr<T[], FreeDel> host_array(int64_t n) {
+    return std::unique_ptr<T[], FreeDel>(static_cast<T *>(malloc((size_t)std::max<int64_t>(n, 1) * sizeof(T))));
+}
+
+// Pinned staging buffers (kPinQuads * 80 B, two per handle: create's H2D ring
+// and the getters' D2H ring) come from a process-wide pool, so that a handle
+// does not pay cudaMallocHost's page pinning when an earlier handle of the
+// process already did.  A destroyed handle returns its buffers (after their
+// last copy completed).  Pinned memory is portable across devices under
+// unified addressing.  SPFOM_NO_PIN_POOL=1: a fresh allocation every time.
+static std::mutex g_pin_mu;
+static std::vector<void *> g_pin_free;
+static cudaError_t pin_take(double **p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        if (!g_pin_free.empty() && !getenv("SPFOM_NO_PIN_POOL")) {
+            *p = static_cast<double *>(g_pin_free.back());
+            g_pin_free.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(reinterpret_cast<void **>(p), bytes);
+}
+static void pin_give(double *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(p);
+}
+
 // Bin = (G lanes per segment, Q quads per lane) -> capacity 4 G Q entries.
 // E > 0: the full-sweep stream kernel maps E entries per lane on G lanes
 // (rows of up to E G entries, StreamLayout); the other kernels use (G, Q).
@@ -255,7 +290,7 @@ struct spfom_handle {
     int64_t L = 0;                                                  // resources (bundles / NRM), 0 = none
     std::vector<int32_t> bptr_h, bres_h;                            // relabelled bundle CSR (set_state)
     std::vector<int32_t> new2old, old2new;     // products
-    std::unique_ptr<int32_t[]> pos_map;        // original entry -> padded entry [nnz] (no zero-fill; < 2^31 by validation)
+    std::unique_ptr<int32_t[], FreeDel> pos_map;   // original entry -> padded entry [nnz] (no zero-fill; < 2^31 by validation)
     std::vector<int32_t> sorder;               // device segment slot -> local segment (bin order)
     std::vector<int64_t> seg_off;              // original CSR offsets (base rows) [m + 1]
     std::vector<int32_t> qoff_h;               // device-order quad offsets [m + 1] (host copy)
@@ -1080,7 +1115,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         destroy_timed(h);
         for (int c = 0; c < 2; ++c) {
             if (h->pin_ev[c]) cudaEventSynchronize(h->pin_ev[c]);
-            if (h->pin[c]) cudaFreeHost(h->pin[c]);
+            pin_give(h->pin[c]);
             if (h->pin_ev[c]) cudaEventDestroy(h->pin_ev[c]);
         }
         if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -1204,9 +1239,12 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     }
     const int64_t nq = qoff[m];
     const int64_t T = h->T;
-    std::vector<double2> segc(std::max<int64_t>(T * m, 1));
-    std::vector<double4> segv(std::max<int64_t>(T * m, 1));
-    h->pos_map.reset(new int32_t[std::max<int64_t>(in->nnz, 1)]);
+    auto segc = host_array<double2>(T * m);   // every slot written below
+    auto segv = host_array<double4>(T * m);
+    h->pos_map = host_array<int32_t>(in->nnz);
+    if (!segc || !segv || !h->pos_map) { h->err = "host allocation"; return bail(SPFOM_ENOMEM); }
+    ptimer.mark("qoff + host arrays");
+    double t_wait = 0.0, t_build = 0.0;
     h->seg_off.assign(in->seg_ptr, in->seg_ptr + m + 1);
     bool bad_numeric = false;
     // The padded arrays (ids, v, omega) are built chunk by chunk of device
@@ -1215,12 +1253,13 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     // pageable staging of the whole instance, no serial H2D afterwards).  The
     // same pinned ring later stages the getters' D2H copies.
     for (int c = 0; c < 2; ++c) {
-        if (cudaMallocHost(reinterpret_cast<void **>(&h->pin[c]), kPinQuads * 80) != cudaSuccess ||
+        if (pin_take(&h->pin[c], kPinQuads * 80) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->pin_ev[c], cudaEventDisableTiming) != cudaSuccess) {
             h->err = "pinned staging";
             return bail(SPFOM_ENOMEM);
         }
     }
+    ptimer.mark("pinned staging ring");
     char *d_pidx = h->ws + h->pl.off[O_PIDX], *d_v = h->ws + h->pl.off[O_V], *d_om = h->ws + h->pl.off[O_OM];
     bool copy_ok = true;
     int64_t chunk_no = 0;
@@ -1229,7 +1268,10 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         while (k1 < m && (int64_t)qoff[k1 + 1] - qoff[k0] <= kPinQuads) ++k1;
         const int64_t q0 = qoff[k0], nqc = (int64_t)qoff[k1] - q0;   // <= kPinQuads (rows <= kMaxQuads)
         const int c = (int)(chunk_no & 1);
+        const double tw0 = PhaseTimer::now();
         if (chunk_no >= 2 && cudaEventSynchronize(h->pin_ev[c]) != cudaSuccess) copy_ok = false;   // buffer free again
+        const double tw1 = PhaseTimer::now();
+        t_wait += tw1 - tw0;
         char *buf = reinterpret_cast<char *>(h->pin[c]);
         int32_t *pidx = reinterpret_cast<int32_t *>(buf);                 // [4 nqc]
         double *vv = reinterpret_cast<double *>(buf + 16 * nqc);           // [4 nqc]
@@ -1281,6 +1323,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
             if (!std::isfinite(vt0)) bad_numeric = true;
         }
         }
+        t_build += PhaseTimer::now() - tw1;
         if (nqc > 0) {
             copy_ok = copy_ok && cudaMemcpyAsync(d_pidx + 16 * q0, pidx, nqc * 16, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
                       cudaMemcpyAsync(d_v + 32 * q0, vv, nqc * 32, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
@@ -1299,6 +1342,7 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
         h->bin_uniform[b] = kBins[b].E > 0 && kBins[b].G == 4 && k1 > k0 &&
                             (int64_t)qoff[k1] - qoff[k0] == (k1 - k0) * kBins[b].E;
     }
+    if (ptimer.on) fprintf(stderr, "[spfom_create]   (chunk builds %.1f ms, waits for the H2D ring %.1f ms)\n", t_build * 1e3, t_wait * 1e3);
     ptimer.mark("padded CSR (omp)");
     // ---- sampled block tables: per (iteration, bin) lists of device slots
     if (pl.sampled) {
@@ -1344,8 +1388,8 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
     };
     std::vector<double> y0(std::max<int64_t>(T * m, 1));
     for (int64_t k = 0; k < T * m; ++k) y0[k] = segv[k].x;
-    bool ok = H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.data(), T * m * 16) &&
-              H2D(O_SEGV, segv.data(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), D1 * 8) &&
+    bool ok = H2D(O_QOFF, qoff.data(), (m + 1) * 4) && H2D(O_SEGC, segc.get(), T * m * 16) &&
+              H2D(O_SEGV, segv.get(), T * m * 32) && H2D(O_R, r.data(), (N + 1) * 8) && H2D(O_C, c.data(), D1 * 8) &&
               H2D(O_TAU, tau.data(), D1 * 8) && H2D(O_G, r.data(), (N + 1) * 8) &&
               H2D(O_ORIG, h->new2old.data(), N * 4);
     h->bptr_h = bptr_d;
@@ -1629,7 +1673,7 @@ static spfom_status fetch_primal(spfom_handle *h, const double *dy, const double
         CUDA_TRY(h, cudaMemcpy2DAsync(t0.data(), 8, dy0, pitch0, 8, T * m, cudaMemcpyDeviceToHost, h->stream));
     if (y && h->nq) {
         for (int c = 0; c < 2; ++c) {
-            if (!h->pin[c]) CUDA_TRY(h, cudaMallocHost(reinterpret_cast<void **>(&h->pin[c]), kPinQuads * 80));
+            if (!h->pin[c]) CUDA_TRY(h, pin_take(&h->pin[c], kPinQuads * 80));
             if (!h->pin_ev[c]) CUDA_TRY(h, cudaEventCreateWithFlags(&h->pin_ev[c], cudaEventDisableTiming));
         }
         // chunks: (period t, device slots [k0, k1)) with at most kPinQuads quads
@@ -2112,7 +2156,8 @@ void spfom_destroy(spfom_handle *h) {
     }
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     for (int c = 0; c < 2; ++c) {
-        if (h->pin[c]) cudaFreeHost(h->pin[c]);
+        if (h->pin_ev[c]) cudaEventSynchronize(h->pin_ev[c]);   // last copy through the buffer done
+        pin_give(h->pin[c]);
         if (h->pin_ev[c]) cudaEventDestroy(h->pin_ev[c]);
     }
     if (h->own_stream) cudaStreamDestroy(h->stream);

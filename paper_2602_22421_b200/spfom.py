@@ -233,9 +233,8 @@ class Solver:
         argument; the solver keeps a reference).
         workspace_offset_bytes > 0: a device allocation of that size is made
         (and kept for the solver's lifetime) before the workspace, which then
-        lands above it -- measured on B200, a workspace in the low part of
-        device memory makes the primal kernel 0-15% slower, run to run
-        (DESIGN.md §9); bench.py uses 32 GiB."""
+        lands above it -- a placement probe only: round 2 measured K1 the same
+        at every offset from 0 to 96 GiB, and bench.py passes 0."""
         import torch  # device memory and streams only
 
         L = load_library()
