@@ -222,11 +222,14 @@ spfom_status spfom_workspace_bytes(const spfom_instance *inst, const spfom_param
  * eta = 0, s = 0 (reading c10).  cuda_stream: cudaStream_t; NULL (or the
  * legacy default stream, which cannot be graph-captured) => the handle creates
  * and owns a private non-blocking stream.  workspace: 256-byte aligned device
- * pointer of >= spfom_workspace_bytes() bytes.  The handle also owns a 40 MB
- * pinned host staging ring (cudaMallocHost): the padded CSR is built into it
- * chunk by chunk and uploaded while the next chunk is built, and the getters
- * stage their device->host copies through it.  SPFOM_ENOMEM if it cannot be
- * allocated. */
+ * pointer of >= spfom_workspace_bytes() bytes.  The handle also holds a 40 MB
+ * pinned host staging ring (two cudaMallocHost buffers): the padded CSR is
+ * built into it chunk by chunk and uploaded while the next chunk is built, and
+ * the getters stage their device->host copies through it.  The buffers come
+ * from a process-wide pool: spfom_destroy returns them (after their last copy
+ * completed) for the next handle, and the pool is not released before the
+ * process exits (SPFOM_NO_PIN_POOL=1: always allocate fresh).  SPFOM_ENOMEM if
+ * the ring cannot be allocated. */
 spfom_status spfom_create(const spfom_instance *inst, const spfom_params *params,
                           const spfom_dist *dist, void *cuda_stream, void *workspace,
                           size_t workspace_bytes, spfom_handle **out);
@@ -312,6 +315,9 @@ spfom_status spfom_step_timed(spfom_handle *h, int64_t k, double *ms);
 
 int64_t spfom_iteration(const spfom_handle *h);
 const char *spfom_last_error(const spfom_handle *h); /* NULL handle => thread's last create error */
+/* Frees the handle (graphs, streams, events, the NCCL communicator); the
+ * pinned staging ring goes back to the process-wide pool (spfom_create).  The
+ * caller's workspace is not touched. */
 void spfom_destroy(spfom_handle *h);
 
 /* --- host-side helpers (no GPU needed) ------------------------------------- */
