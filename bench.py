@@ -94,7 +94,7 @@ def ncu_traffic(workload: str, kernel="k_primal"):
         return None
     try:
         d = json.load(open(p))
-        e = d.get(kernel, {})
+        e = d.get(kernel if workload == "huge" else f"{kernel}@{workload}", {})
         if e.get("workload", "huge") != workload:
             return None
         return e.get("dram_bytes_per_launch")

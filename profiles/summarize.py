@@ -6,7 +6,8 @@
 writes profiles/<ROUND>_k1_full.txt (key metrics, stall reasons, instruction
 mix), profiles/<ROUND>_launches.csv (the per-launch list) and updates
 profiles/ncu_summary.json (DRAM bytes per K1 launch, read by bench.py's
-roofline.traffic).
+roofline.traffic; key k_primal for huge, k_primal@<WORKLOAD> for the other
+configs -- set WORKLOAD=medium|multi when summarising their captures).
 """
 import collections
 import csv
@@ -183,9 +184,10 @@ def main():
     wr = float(m["dram__bytes_write.sum"][0]) * UNIT[m["dram__bytes_write.sum"][1]]
     summ_path = os.path.join(HERE, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    summ["k_primal"] = {"round": rnd, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+    wl = os.environ.get("WORKLOAD", "huge")
+    summ["k_primal" if wl == "huge" else f"k_primal@{wl}"] = {"round": rnd, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                         "duration": m["gpu__time_duration.sum"], "source": os.path.basename(rep),
-                        "workload": os.environ.get("WORKLOAD", "huge")}
+                        "workload": wl}
     json.dump(summ, open(summ_path, "w"), indent=1)
     if launches:
         shutil.copy(launches, os.path.join(HERE, f"{rnd}_launches.csv"))
