@@ -374,6 +374,40 @@ def test_step_timed_is_step():
     b.close()
 
 
+def test_pinned_pool_reuse_across_handles():
+    """The pinned staging ring comes from a process-wide pool (spfom_create):
+    handles alive together hold distinct buffers, a destroyed handle's buffers
+    serve the next one, and create's layout and the getters' D2H through reused
+    buffers give the same iterates (multi-chunk instance: > 2^18 quads), up to
+    the rounding order of the usage reductions."""
+    import threading
+    from paper_2602_22421_b200 import Solver
+    inst = generate("medium", m=12000, N=3000, k=(20, 200))    # ~1.3 M entries: several ring chunks
+    ref = Solver(inst, _params())
+    ref.step(6)
+    y_ref, y0_ref = ref.primal()
+    eta_ref = ref.duals()
+    ref.close()                                                # its buffers go back to the pool
+    out = {}
+
+    def run(key):
+        s = Solver(inst, _params())
+        s.step(6)
+        out[key] = (s.primal(), s.duals())
+        s.close()
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert sorted(out) == [0, 1, 2]
+    # equal up to the rounding order of the usage reductions (fp64 atomics):
+    # a buffer shared by two live handles would differ at O(1)
+    for (y, y0), eta in out.values():
+        assert rel_inf(y, y_ref, 1.0) <= 1e-12 and rel_inf(y0, y0_ref, 1.0) <= 1e-12
+        assert rel_inf(eta, eta_ref, 1.0) <= 1e-12
+
+
 # ------------------------------------------------------------ accuracy gates
 @pytest.mark.parametrize("seed", [1, 11, 12])
 def test_tiny_accuracy_vs_dense_lp(seed):
