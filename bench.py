@@ -95,7 +95,7 @@ def ncu_traffic(workload: str, kernel="k_primal"):
     try:
         d = json.load(open(p))
         e = d.get(kernel if workload == "huge" else f"{kernel}@{workload}", {})
-        if e.get("workload", "huge") != workload:
+        if e.get("workload", "huge") != workload or not e.get("covers_k1", True):
             return None
         return e.get("dram_bytes_per_launch")
     except Exception:

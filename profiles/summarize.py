@@ -187,7 +187,10 @@ def main():
     wl = os.environ.get("WORKLOAD", "huge")
     summ["k_primal" if wl == "huge" else f"k_primal@{wl}"] = {"round": rnd, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                         "duration": m["gpu__time_duration.sum"], "source": os.path.basename(rep),
-                        "workload": wl}
+                        "workload": wl,
+                        # COVERS_K1=0: the capture is one of several concurrent bin launches
+                        # (medium), so its bytes are not the K1 step's traffic
+                        "covers_k1": os.environ.get("COVERS_K1", "1") == "1"}
     json.dump(summ, open(summ_path, "w"), indent=1)
     if launches:
         shutil.copy(launches, os.path.join(HERE, f"{rnd}_launches.csv"))
