@@ -447,17 +447,22 @@ def main():
     traffic = ncu_traffic(args.config)
 
     # e2e through the public API with host buffers: create (H2D) + K steps + duals/primal (D2H)
-    barrier()
-    torch.cuda.synchronize(device)
-    t0 = time.perf_counter()
-    s2 = Solver(shard, params, **kw)
-    s2.step(args.steps)
-    eta = s2.duals()
-    y, y0 = s2.primal()
-    t1 = time.perf_counter()
-    e2e_info = s2.info()
-    s2.close()
-    e2e_s = max_over_ranks(t1 - t0)
+    # (three independent repetitions, each from the host arrays; the median is reported)
+    e2e_reps = []
+    for _ in range(3):
+        barrier()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        s2 = Solver(shard, params, **kw)
+        s2.step(args.steps)
+        eta = s2.duals()
+        y, y0 = s2.primal()
+        t1 = time.perf_counter()
+        e2e_info = s2.info()
+        s2.close()
+        del eta, y, y0
+        e2e_reps.append(max_over_ranks(t1 - t0))
+    e2e_s = sorted(e2e_reps)[1]
     e2e_value = args.steps / e2e_s
     nq = e2e_info["nnz_padded"] // 4
     h2d = nq * (16 + 32 + 32) + (shard.m + 1) * 4 + shard.m * (16 + 8 + 32 + 4) + (shard.N + 1) * 8 * 4
@@ -502,7 +507,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                     "d2h_bytes_per_step": d2h / args.steps,
                     "definition": "wall time of Solver(host arrays) [validate+layout+H2D] + K graph-replayed "
-                                  "iterations + duals()+primal() D2H, through the C ABI"},
+                                  "iterations + duals()+primal() D2H, through the C ABI; median of 3 repetitions",
+                    "reps_s": [round(x, 4) for x in e2e_reps]},
             "gpu_launches": int(info["launches_per_iteration"]) * args.steps,
             "cpu_baseline": cpu_baseline,
             "residuals_after": {k: res[k] for k in ("iteration", "rel_gap", "infeas_rel", "newton_failures",
