@@ -38,3 +38,5 @@ for lib in sys.argv[1:]:
     r = subprocess.run([sys.executable, __file__, "--child"], env=env, capture_output=True, text=True)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-600:]
     print(f"{os.path.basename(lib):24s} {line}", flush=True)
+    if os.environ.get("SHOW_BINS"):      # -DSPFOM_DIAG_BIN_SMS libraries: the bins' weights and SM shares
+        print("".join(sorted(set(l + "\n" for l in r.stderr.splitlines() if l.startswith("[spfom] bin")))), end="", flush=True)

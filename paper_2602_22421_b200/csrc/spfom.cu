@@ -1523,6 +1523,20 @@ spfom_status spfom_create(const spfom_instance *in, const spfom_params *p, const
                       cudaEventCreateWithFlags(&h->ev_join[b], cudaEventDisableTiming) == cudaSuccess;
             }
             if (!okc) { h->err = "side stream creation failed"; return bail(SPFOM_ECUDA); }
+#ifdef SPFOM_DIAG_BIN_SMS
+            // diagnostic (exp/run_shares.sh): SM shares of the active bins from the environment, "a,b,c,.."
+            if (const char *ov = getenv("SPFOM_BIN_SMS")) {
+                for (int b = 0; b < kNumBins; ++b) {
+                    if (w[b] == 0) continue;
+                    h->bin_sms[b] = std::max(1, atoi(ov));
+                    const char *c = strchr(ov, ',');
+                    if (!c) break;
+                    ov = c + 1;
+                }
+            }
+            for (int b = 0; b < kNumBins; ++b)
+                if (w[b]) fprintf(stderr, "[spfom] bin %d: w %lld sms %d\n", b, (long long)w[b], h->bin_sms[b]);
+#endif
         }
     }
     ptimer.mark("H2D + state + modes");
